@@ -1,0 +1,171 @@
+/*
+ * blfmm_gpu.h — C ABI of the B200-native band-limited FMM RBF matvec.
+ *
+ * Drop-in boundary for the reference library blfmm (/root/reference/proj/core).
+ * Plain pointers and sizes only; no CUDA or torch types in the signatures
+ * (streams are passed as void*). Every entry point returns a status code and
+ * leaves a thread-local message for blfmm_last_error().
+ *
+ * Reference interfaces replaced (file:line under /root/reference/proj/core):
+ *   blfmm_plan_create   build_tree(const PointSet&, int)        include/blfmm/geometry.hpp:72
+ *                       + make_level_grids(kernel, sigma_leaf, m_leaf, d,
+ *                         leaf_level, GridMode, stencil_k)      include/blfmm/mlfmm.hpp:61-63
+ *                       (the immutable BoxTree / LevelGrids pair a caller
+ *                        builds once and reuses, solver.cpp:280-293)
+ *   blfmm_execute       SumResult mlfmm_matvec(const SumRequest&, const BoxTree&,
+ *                         const LevelGrids&)                    include/blfmm/mlfmm.hpp:98-99
+ *   blfmm_execute_single SumResult fmm_matvec_single(const SumRequest&,
+ *                         const BoxTree&)                       include/blfmm/fmm.hpp:55
+ *   blfmm_direct        SumResult direct_matvec(kernel, ps, weights,
+ *                         use_bandlimited=false, ...)           include/blfmm/fmm.hpp:33-36
+ *   blfmm_parse_kernel_spec  RadialKernel parse_kernel_spec(const std::string&)
+ *                                                               include/blfmm/kernels.hpp:23
+ *   blfmm_translation_coefficients  translation_coefficients(k, grid, spectral)
+ *                                                               include/blfmm/bandlimit.hpp:106-108
+ *   blfmm_get_expansions upsweep / couple / downsweep stage outputs
+ *                                                               include/blfmm/mlfmm.hpp:79-94
+ *   status codes        std::invalid_argument / std::domain_error /
+ *                       blfmm::accuracy_error                   include/blfmm/common.hpp:33-41
+ */
+#ifndef BLFMM_GPU_H
+#define BLFMM_GPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLFMM_GPU_ABI_VERSION 1
+
+/* Status codes (reference exception class in parentheses). */
+enum blfmm_status {
+  BLFMM_OK = 0,
+  BLFMM_EINVAL = 1,    /* std::invalid_argument                       */
+  BLFMM_EDOMAIN = 2,   /* std::domain_error (unsupported d / kernel)  */
+  BLFMM_EACCURACY = 3, /* blfmm::accuracy_error; see blfmm_last_error_value */
+  BLFMM_ECUDA = 4,     /* CUDA runtime error, or no usable device     */
+  BLFMM_ENCCL = 5,     /* multi-GPU exchange error                    */
+  BLFMM_ENOMEM = 6     /* device allocation failed                    */
+};
+
+/* RadialKernel::type (kernels.hpp:12-17); only the band-limited FMM kernels
+ * of the north star are executable on the GPU path. */
+enum blfmm_kernel_type {
+  BLFMM_KERNEL_GAUSSIAN = 0, /* phi = exp(-c r^2)      */
+  BLFMM_KERNEL_MQ = 1,       /* phi = sqrt(r^2 + c^2)  */
+  BLFMM_KERNEL_IMQ = 2,      /* phi = 1/sqrt(r^2+c^2)  */
+  BLFMM_KERNEL_TPS = 3,      /* parsed, EDOMAIN on the GPU path */
+  BLFMM_KERNEL_WENDLAND_C2 = 4,
+  BLFMM_KERNEL_WENDLAND31 = 5
+};
+
+/* GridMode (mlfmm.hpp:21-28). Only `shared` is executable (EDOMAIN else). */
+enum blfmm_grid_mode { BLFMM_GRID_SHARED = 0, BLFMM_GRID_SCALED = 1 };
+
+typedef struct blfmm_plan blfmm_plan;
+
+typedef struct blfmm_plan_desc {
+  int d;                  /* 1, 2 or 3 */
+  long long n;            /* number of points (>= 0) */
+  const double* coords;   /* HOST, n*d doubles, AoS (x0,y0,[z0],x1,...) caller order */
+  double domain_lo[3];    /* BoundingBox::lo (geometry.hpp:10-14); unused axes ignored */
+  double domain_hi[3];    /* BoundingBox::hi */
+  int kernel_type;        /* enum blfmm_kernel_type */
+  double kernel_shape;    /* c (Gaussian c = eps^2) */
+  double sigma;           /* leaf band limit (> 0) */
+  int m_per_dim;          /* quadrature nodes per axis M (>= 2); K = M^d */
+  int leaf_level;         /* uniform tree depth L (>= 2, d*L <= 24) */
+  int grid_mode;          /* enum blfmm_grid_mode */
+  int stencil_k;          /* scaled-mode stencil (ignored for shared) */
+  int nrhs;               /* right-hand sides per execute (>= 1) */
+  int device;             /* CUDA device ordinal, -1 = current */
+  const double* c_table;  /* optional HOST override of C(xi_m), K doubles
+                             (LowRankFactors::c_vals); NULL = compute */
+  int rank;               /* multi-GPU: this plan's Morton-range index ... */
+  int world;              /* ... of `world` ranges (1 = whole problem) */
+} blfmm_plan_desc;
+
+/* SumStats (fmm.hpp:10-14). */
+typedef struct blfmm_stats {
+  long long near_pairs;
+  long long far_work;
+  double max_imag_residual;
+} blfmm_stats;
+
+/* Plan facts (sizes of the device-resident tree and expansion sets). */
+typedef struct blfmm_plan_info {
+  int d, m_per_dim, leaf_level, nrhs;
+  long long n, K;
+  long long boxes[25];      /* nonempty boxes per level 0..L (levels >= 2 used) */
+  long long near_pairs;     /* of the owned targets */
+  long long far_work;       /* reference formula, mlfmm.cpp:398-404 */
+  long long far_work_single;/* fmm.cpp:152,179,209 */
+  long long il_pairs;       /* nonempty (target, source) IL pairs, all levels */
+  long long owned_begin, owned_end; /* owned sorted-point range (multi-GPU) */
+  double plan_seconds;
+  long long device_bytes;
+} blfmm_plan_info;
+
+/* Per-stage device times of the last execute (CUDA events on the launch
+ * stream), enabled by blfmm_set_profiling. Order: tree/gather, p2m, m2m,
+ * m2l(+l2l), l2p, near, combine. */
+#define BLFMM_NSTAGES 7
+typedef struct blfmm_stage_times {
+  double ms[BLFMM_NSTAGES];
+  int launches[BLFMM_NSTAGES];
+} blfmm_stage_times;
+
+const char* blfmm_last_error(void);
+double blfmm_last_error_value(void); /* accuracy_error::achieved() */
+int blfmm_abi_version(void);
+
+/* parse_kernel_spec grammar: "name[:key=value]", case-insensitive. */
+int blfmm_parse_kernel_spec(const char* spec, int* kernel_type, double* shape);
+
+/* Host plan-time translation spectrum, K = M^d doubles in make_quadrature's
+ * row-major node order. */
+int blfmm_translation_coefficients(int d, int kernel_type, double shape,
+                                   double sigma, int m_per_dim, double* c_out);
+
+int blfmm_plan_create(const blfmm_plan_desc* desc, blfmm_plan** out);
+int blfmm_plan_destroy(blfmm_plan* plan);
+int blfmm_plan_get_info(const blfmm_plan* plan, blfmm_plan_info* info);
+
+/* One matvec with HOST buffers: lambda [nrhs][n] (rhs-major, caller point
+ * order), out [nrhs][n]. H2D / D2H copies are part of the call. stream may be
+ * NULL (the plan's own stream). Synchronises before returning. */
+int blfmm_execute(blfmm_plan* plan, const double* lambda, double* out,
+                  blfmm_stats* stats, void* stream);
+
+/* Same with DEVICE buffers (no copies, no synchronisation; stats may be NULL
+ * to avoid the D2H read of max_imag_residual). */
+int blfmm_execute_device(blfmm_plan* plan, const double* d_lambda,
+                         double* d_out, blfmm_stats* stats, void* stream);
+
+/* fmm_matvec_single semantics (single-level sum, which the shared-grid
+ * multilevel sweep equals to rounding, mlfmm.hpp:17-20); stats.far_work uses
+ * the single-level count. HOST buffers. */
+int blfmm_execute_single(blfmm_plan* plan, const double* lambda, double* out,
+                         blfmm_stats* stats, void* stream);
+
+/* Stage expansions of one level, dense reference box-id order (row-major),
+ * out[(box*K + node)*2 + {re,im}] for right-hand side `rhs`, zeros for empty
+ * boxes. kind 0 = multipoles (upsweep), 1 = couple() locals before L2L (needs
+ * blfmm_set_keep_couple(plan,1) before the execute), 2 = locals after L2L.
+ * Reflects the last execute. */
+int blfmm_get_expansions(blfmm_plan* plan, int level, int kind, int rhs,
+                         double* out);
+int blfmm_set_keep_couple(blfmm_plan* plan, int enable);
+
+int blfmm_set_profiling(blfmm_plan* plan, int enable);
+int blfmm_get_stage_times(const blfmm_plan* plan, blfmm_stage_times* t);
+
+/* Independent O(N^2) check (direct_matvec, fmm.cpp:30-75): values for
+ * n_targets target indices (NULL = all n) into HOST out. */
+int blfmm_direct(int d, long long n, const double* coords, int kernel_type,
+                 double shape, const double* lambda, long long n_targets,
+                 const long long* targets, double* out, int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLFMM_GPU_H */

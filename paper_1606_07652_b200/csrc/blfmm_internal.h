@@ -1,0 +1,30 @@
+// Internal declarations shared by the host plan code and the CUDA sources.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/blfmm_gpu.h"
+
+namespace blfmm_gpu {
+
+struct Error : std::runtime_error {
+  int code;
+  double achieved = 0.0;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+struct KernelSpec {
+  int type = BLFMM_KERNEL_GAUSSIAN;
+  double shape = 1.0;
+};
+
+KernelSpec parse_spec(const std::string& spec);
+void require_fmm_kernel(const KernelSpec& k);
+double fourier_value(const KernelSpec& k, double xi, int d);
+std::vector<double> translation_spectrum(const KernelSpec& k, double sigma,
+                                         int m, int d);
+
+}  // namespace blfmm_gpu

@@ -1,0 +1,57 @@
+"""Generates tests/golden/*.npz from the REFERENCE ITSELF (oracle/_ref, the
+reference's own sources compiled with the repo's Boost.Math shim).
+
+Run in the build container (needs /root/reference):
+    make -C oracle && python tests/golden/make_golden.py
+The fixtures are small and committed; the GPU box never reads /root/reference.
+"""
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from oracle import pyoracle as po  # noqa: E402
+from paper_1606_07652_b200 import inputs as I  # noqa: E402
+
+
+def mlfmm_fixture(name, x, w, spec, sigma, m, leaf, with_direct=False):
+    v, st = po.ref_mlfmm(x, w, spec, sigma, m, leaf)
+    extra = {}
+    if with_direct:
+        dv, _ = po.ref_direct(x, w, spec)
+        extra["direct"] = dv
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), kind="mlfmm", x=x, w=w, spec=spec,
+                        sigma=sigma, m=m, leaf=leaf, values=v, near_pairs=st["near_pairs"],
+                        far_work=st["far_work"], max_imag=st["max_imag_residual"], **extra)
+    print(name, x.shape, st)
+
+
+def main():
+    assert po.ref_available(), "build oracle/_ref first (make -C oracle)"
+    W = I.WORKLOADS["P1"]
+    x, w = W.make()
+    mlfmm_fixture("p1_gaussian_2d_ref", x, w, W.kernel, W.sigma, W.m, W.leaf, with_direct=True)
+    W = I.WORKLOADS["P1b"]
+    x, w = W.make()
+    mlfmm_fixture("p1b_gaussian_2d_bandcapture_ref", x, w, W.kernel, W.sigma, W.m, W.leaf,
+                  with_direct=True)
+    W = I.WORKLOADS["P4"]
+    x, w = W.make(8192)
+    mlfmm_fixture("p4_mq_2d_small_ref", x, w, W.kernel, W.sigma, W.m, 4)
+    x = I.generate_quasiuniform(256, 2, 77, 0.4)
+    w = I.uniform_weights(256, 8)
+    mlfmm_fixture("telescope_imq_2d_ref", x, w, "imq:c=1", math.pi, 12, 3)
+    x = I.uniform_points(2048, 2, 31)
+    w = I.uniform_weights(2048, 32)
+    mlfmm_fixture("imq_2d_small_ref", x, w, "imq:c=0.1", math.pi, 16, 4)
+    x = I.generate_quasiuniform(1024, 1, 2026, 0.35)
+    w = I.uniform_weights(1024, 99)
+    mlfmm_fixture("imq_1d_ref", x, w, "imq:c=1", math.pi, 64, 5)
+
+
+if __name__ == "__main__":
+    main()

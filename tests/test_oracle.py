@@ -1,0 +1,298 @@
+"""Pins the CPU oracle (test infrastructure) before it is trusted.
+
+1. Against the reference tests' own golden values and hand fixtures
+   (file:line cited per test, /root/reference/proj/tests/...).
+2. Against the reference itself compiled from its sources (oracle/_ref),
+   d <= 2, when that library is present.
+3. For d = 3 (no reference counterpart): algebraic invariants of the
+   restatement and independent quadrature of the 3-D translation spectrum.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+from paper_1606_07652_b200 import inputs as I
+
+
+def rel_linf(a, b):
+    return np.abs(a - b).max() / np.abs(b).max()
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+# --------------------------------------------------------------- goldens
+def test_rng_matches_reference_hash(oracle):
+    # common.hpp:45-55 restated in numpy == the C restatement
+    for seed, ctr in [(0, 0), (1, 2), (2026, 99), (2 ** 63 + 5, 12345)]:
+        assert I.uniform01(seed, ctr) == oracle.lib().orc_uniform01(seed, ctr)
+
+
+def test_direct_three_point_hand_fixture(oracle):
+    # test_fmm.cpp:37-49
+    x = np.array([[0.0], [0.5], [2.0]])
+    w = np.array([1.0, 2.0, -1.0])
+    v = oracle.direct(x, w, "gaussian:c=1")
+    want = [2.5392859272540756, 2.6734015585095405, -0.77088591198753715]
+    np.testing.assert_allclose(v, want, rtol=1e-15)
+
+
+@pytest.mark.parametrize("spec,xi,d,want,tol", [
+    # test_kernels.cpp:123-153 frozen transforms
+    ("gaussian:c=1", 1.0, 1, 1.380388447043143, 1e-14),
+    ("gaussian:c=1", 1.0, 2, 2.4466748187071037, 1e-14),
+    ("gaussian:c=2", 1.5, 1, 0.9460511445784283, 1e-14),
+    ("imq:c=1", 1.0, 1, 0.84204887648141667, 1e-13),
+    ("imq:c=1", 1.0, 2, 2.3114546995818434, 1e-14),
+    ("imq:c=2", 1.5, 1, 0.069479008772558496, 1e-13),
+    ("mq:c=1", 1.0, 1, -1.2038144603944691, 1e-13),
+    ("mq:c=1", 2.0, 2, -0.31887624869072725, 1e-14),
+])
+def test_eval_fourier_frozen(oracle, spec, xi, d, want, tol):
+    assert abs(oracle.eval_fourier(spec, xi, d) - want) <= tol * abs(want)
+
+
+def test_fourier_singular_at_origin_raises(oracle):
+    # test_kernels.cpp:166-175: singular spectra throw domain_error at 0
+    for spec in ("imq:c=1", "mq:c=1"):
+        with pytest.raises(oracle.OracleError) as e:
+            oracle.eval_fourier(spec, 0.0, 2)
+        assert e.value.code == 2
+    assert abs(oracle.eval_fourier("gaussian:c=1", 0.0, 1) - math.sqrt(math.pi)) < 1e-15
+
+
+def test_c_table_frozen_gaussian(oracle):
+    # test_bandlimit.cpp:207-217
+    c = oracle.c_table("gaussian:c=1", 2.0, 4, 1)
+    assert abs(c[3] - 0.2196956447338612) <= 1e-13 * 0.2196956447338612
+    assert abs(c[1] - c[3]) <= 1e-13 * c[3]
+    assert abs(c[2] - math.sqrt(math.pi) / (2 * math.pi)) <= 1e-13
+
+
+def test_c_table_imq_1d_cell_average_vs_simpson(oracle):
+    # test_bandlimit.cpp:237-251 (node 5 covers [pi/4, pi/2])
+    c = oracle.c_table("imq:c=1", math.pi, 8, 1)
+    lo, hi = -math.pi + 5 * (2 * math.pi / 8), -math.pi + 6 * (2 * math.pi / 8)
+    n = 20000
+    h = (hi - lo) / n
+    a = lo + h * np.arange(n)
+    spec = np.vectorize(lambda xi: oracle.eval_fourier("imq:c=1", xi, 1) / (2 * math.pi))
+    acc = (h / 6.0 * (spec(a) + 4.0 * spec(a + h / 2) + spec(a + h))).sum()
+    assert abs(c[5] - acc / (hi - lo)) <= 1e-11 * abs(c[5])
+    # pole cell stays finite and dominates its midpoint sample
+    mid = oracle.eval_fourier("imq:c=1", (4 - 4) + 0.5 * (2 * math.pi / 8), 1) / (2 * math.pi)
+    assert np.isfinite(c[4]) and c[4] > mid
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_shared_grids_telescope(oracle, d):
+    # test_mlfmm.cpp:321-334: multilevel == single level to 1e-12
+    n, leaf, m = 256, (4 if d == 1 else 3), (32 if d == 1 else 12)
+    x = I.generate_quasiuniform(n, d, 77, 0.4)
+    w = I.uniform_weights(n, 8)
+    ml, st, _ = oracle.mlfmm(x, w, "imq:c=1", math.pi, m, leaf)
+    sl, st2 = oracle.single(x, w, "imq:c=1", math.pi, m, leaf)
+    assert rel_linf(ml, sl) < 1e-12
+    assert st["near_pairs"] == st2["near_pairs"]
+
+
+def test_unit_source_at_leaf_center(oracle):
+    # test_mlfmm.cpp:142-158: coefficients exactly 1+0i, empty box exactly 0
+    x = np.array([[0.375]])
+    e = oracle.expansions(x, np.array([1.0]), "gaussian:c=1", math.pi, 8, 2, 2, 0)
+    assert np.all(e[1] == 1.0 + 0.0j)
+    assert np.all(e[0] == 0.0)
+
+
+def test_tree_hand_enumeration_1d(oracle):
+    # test_geometry.cpp:180-206
+    x = I.generate_quasiuniform(16, 1, 0, 0.0)
+    nb = oracle.tree_lists(x, 2, 2, 0)
+    il = oracle.tree_lists(x, 2, 2, 1)
+    assert [list(v) for v in nb] == [[0, 1], [0, 1, 2], [1, 2, 3], [2, 3]]
+    assert [list(v) for v in il] == [[2, 3], [3], [0], [0, 1]]
+
+
+def test_tree_counts_2d(oracle):
+    # test_geometry.cpp:208-226
+    x = I.generate_quasiuniform(64, 2, 0, 0.0)
+    nb = oracle.tree_lists(x, 2, 2, 0)
+    il = oracle.tree_lists(x, 2, 2, 1)
+    assert list(nb[0]) == [0, 1, 4, 5]
+    assert len(nb[5]) == 9 and len(il[0]) == 12 and len(il[5]) == 7
+
+
+def test_leaf_binning_clamp(oracle):
+    # test_geometry.cpp:272-293: leaf_of({0.3,0.8}) == 7, {1,1} clamps to 15
+    x = np.array([[0.3, 0.8], [1.0, 1.0], [0.0, 0.0]])
+    lp = oracle.tree_lists(x, 2, 2, 2)
+    assert list(lp[7]) == [0] and list(lp[15]) == [1] and list(lp[0]) == [2]
+
+
+@pytest.mark.parametrize("d,leaf", [(1, 4), (2, 3), (3, 3)])
+def test_every_leaf_pair_handled_once(oracle, d, leaf):
+    # test_geometry.cpp:246-270, extended to d = 3
+    x = np.full((1, d), 0.5)
+    nbr = [set(v.tolist()) for v in oracle.tree_lists(x, leaf, leaf, 0)]
+    ils = {l: [set(v.tolist()) for v in oracle.tree_lists(x, leaf, l, 1)]
+           for l in range(2, leaf + 1)}
+    nb = 1 << (d * leaf)
+
+    def parent(l, b):
+        n = 1 << l
+        idx = []
+        for _ in range(d):
+            idx.append(b % n)
+            b //= n
+        idx = [i // 2 for i in idx[::-1]]
+        out = 0
+        for i in idx:
+            out = (out << (l - 1)) | i
+        return out
+
+    rng = np.random.default_rng(0)
+    pairs = [(a, b) for a in range(nb) for b in range(nb)] if nb <= 256 else \
+        [tuple(p) for p in rng.integers(0, nb, size=(20000, 2))]
+    for a, b in pairs:
+        handled = 1 if b in nbr[a] else 0
+        aa, bb = a, b
+        for l in range(leaf, 1, -1):
+            if bb in ils[l][aa]:
+                handled += 1
+            aa, bb = parent(l, aa), parent(l, bb)
+        assert handled == 1, (a, b)
+
+
+def test_far_work_dense_il_sum(oracle):
+    # sum_a |IL_l(a)| closed form == explicit list sizes
+    for d, leaf in [(1, 5), (2, 4), (3, 3)]:
+        x = np.full((1, d), 0.5)
+        for l in range(2, leaf + 1):
+            il = oracle.tree_lists(x, leaf, l, 1)
+            assert sum(len(v) for v in il) == oracle.sum_il(d, leaf, l)
+
+
+# ------------------------------------------------- 3-D restatement checks
+def test_telescope_3d(oracle):
+    x = I.uniform_points(1500, 3, 11)
+    w = I.uniform_weights(1500, 12)
+    ml, st, _ = oracle.mlfmm(x, w, "imq:c=0.1", math.pi, 6, 3)
+    sl, st2 = oracle.single(x, w, "imq:c=0.1", math.pi, 6, 3)
+    assert rel_linf(ml, sl) < 1e-12
+    assert st["near_pairs"] == st2["near_pairs"]
+
+
+def test_c_table_3d_gaussian_closed_form(oracle):
+    sigma, m, c = math.pi, 6, 64.0
+    tab = oracle.c_table(f"gaussian:c={c}", sigma, m, 3)
+    ax = -sigma + np.arange(m) * (2 * sigma / m)
+    X = np.stack(np.meshgrid(ax, ax, ax, indexing="ij"), -1).reshape(-1, 3)
+    rho2 = (X ** 2).sum(1)
+    want = (math.pi / c) ** 1.5 * np.exp(-rho2 / (4 * c)) / (2 * math.pi) ** 3
+    np.testing.assert_allclose(tab, want, rtol=1e-14)
+
+
+def test_c_table_3d_imq_independent_quadrature(oracle):
+    """3-D singular C values vs scipy (independent adaptive quadrature)."""
+    from scipy import integrate, special
+    c = 0.1
+    f = lambda z, y, x: 4 * math.pi * c * special.k1(c * math.sqrt(x * x + y * y + z * z)) / \
+        math.sqrt(x * x + y * y + z * z)
+    dxi = 2 * math.pi / 16
+    # a cell away from the pole
+    a = np.array([dxi, 0.0, 2 * dxi])
+    b = a + dxi
+    got = oracle.cell_average("imq:c=0.1", 3, a, b)
+    want = integrate.tplquad(f, a[0], b[0], a[1], b[1], a[2], b[2], epsabs=0, epsrel=1e-12)[0]
+    assert abs(got - want / dxi ** 3) <= 1e-10 * abs(got)
+    # the pole corner cube: integrand ~ 4 pi / rho^2, integrable; compare in
+    # spherical coordinates with scipy on the same excluded-ball domain
+    got0 = oracle.cell_average("imq:c=0.1", 3, np.zeros(3), np.full(3, dxi))
+    g = lambda r, th, ph: r * r * math.sin(th) * 4 * math.pi * c * special.k1(c * r) / r
+    tot = 0.0
+    # 3 pyramids x 2 halves of {phi in [0, pi/4], theta < atan(1/cos phi)}
+    tot = 6 * integrate.tplquad(
+        g, 0, math.pi / 4, 0, lambda ph: math.atan(1 / math.cos(ph)),
+        1e-8, lambda ph, th: dxi / math.cos(th), epsabs=0, epsrel=1e-11)[0]
+    assert abs(got0 - tot / dxi ** 3) <= 1e-9 * abs(got0)
+
+
+# ------------------------------------------------ oracle vs the reference
+needs_ref = pytest.mark.skipif("not __import__('oracle.pyoracle', fromlist=['x']).ref_available()",
+                               reason="oracle/_ref not built (needs /root/reference)")
+
+
+@needs_ref
+@pytest.mark.parametrize("spec,d,m", [("gaussian:c=16", 2, 64), ("gaussian:c=16", 2, 44),
+                                      ("imq:c=0.1", 2, 16), ("mq:c=0.05", 2, 16),
+                                      ("imq:c=1", 2, 12), ("imq:c=1", 1, 8), ("mq:c=1", 1, 32)])
+def test_c_table_matches_reference(oracle, spec, d, m):
+    a = oracle.c_table(spec, math.pi, m, d)
+    b = oracle.ref_c_table(spec, math.pi, m, d)
+    assert np.abs(a - b).max() <= 1e-14 * np.abs(b).max()
+
+
+@needs_ref
+@pytest.mark.parametrize("name,n,leaf", [("P1", 4096, 3), ("P1b", 4096, 3), ("P4", 8192, 4)])
+def test_mlfmm_matches_reference_2d(oracle, name, n, leaf):
+    W = I.WORKLOADS[name]
+    x, w = W.make(n)
+    v, st, _ = oracle.mlfmm(x, w, W.kernel, W.sigma, W.m, leaf)
+    rv, rst = oracle.ref_mlfmm(x, w, W.kernel, W.sigma, W.m, leaf)
+    assert rel_l2(v, rv) <= 1e-14
+    assert st["near_pairs"] == rst["near_pairs"] and st["far_work"] == rst["far_work"]
+    assert abs(st["max_imag_residual"] - rst["max_imag_residual"]) <= 1e-12 * max(1.0, rst["max_imag_residual"])
+
+
+@needs_ref
+def test_stage_expansions_match_reference(oracle):
+    W = I.WORKLOADS["P1"]
+    x, w = W.make(2048)
+    for level in (2, 3):
+        for kind in (0, 1):
+            a = oracle.expansions(x, w, W.kernel, W.sigma, 16, 3, level, kind)
+            b = oracle.ref_expansions(x, w, W.kernel, W.sigma, 16, 3, level, kind)
+            assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max()
+
+
+@needs_ref
+def test_tree_lists_match_reference(oracle):
+    x = I.uniform_points(3000, 2, 5)
+    for l in (2, 3, 4):
+        for which in (0, 1):
+            a = oracle.tree_lists(x, 4, l, which)
+            b = oracle.ref_tree_lists(x, 4, l, which)
+            assert all(np.array_equal(p, q) for p, q in zip(a, b))
+    a = oracle.tree_lists(x, 4, 4, 2)
+    b = oracle.ref_tree_lists(x, 4, 4, 2)
+    assert all(np.array_equal(p, q) for p, q in zip(a, b))
+
+
+@needs_ref
+def test_direct_matches_reference(oracle):
+    x = I.uniform_points(700, 2, 9)
+    w = I.uniform_weights(700, 10)
+    for spec in ("gaussian:c=16", "imq:c=0.1", "mq:c=0.05"):
+        v = oracle.direct(x, w, spec)
+        rv, near = oracle.ref_direct(x, w, spec)
+        assert rel_l2(v, rv) <= 1e-15 and near == 700 * 700
+
+
+def test_golden_fixtures_match_oracle(oracle):
+    """tests/golden/*.npz were produced by the reference itself
+    (tests/golden/make_golden.py); the oracle must reproduce them."""
+    import glob
+    import os
+    files = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+    assert files, "golden fixtures missing"
+    for f in files:
+        g = np.load(f, allow_pickle=False)
+        if str(g["kind"]) != "mlfmm":
+            continue
+        v, st, _ = oracle.mlfmm(g["x"], g["w"], str(g["spec"]), float(g["sigma"]),
+                                int(g["m"]), int(g["leaf"]))
+        assert rel_l2(v, g["values"]) <= 1e-14, f
+        assert st["near_pairs"] == int(g["near_pairs"]) and st["far_work"] == int(g["far_work"])

@@ -1,0 +1,268 @@
+"""GPU parity: the sm_100a path through the C ABI against the oracle (and
+the reference's own outputs for d <= 2) on the same seeded inputs.
+
+Bar (north star): rel-l2 <= 1e-10 in fp64 against the reference CPU FMM with
+identical parameters; near_pairs / far_work exact; stage expansions per
+level; edge cases the reference tests (empty, single point, boundary
+coordinates, empty boxes, leaf level 2, batched right-hand sides).
+"""
+import glob
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_1606_07652_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10  # north-star relative l2 tolerance (fp64)
+
+
+def rel_l2(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def gpu_mlfmm(B, x, w, spec, sigma, m, leaf, lo=None, hi=None, c_table=None):
+    d = x.shape[1]
+    dom = B.BoundingBox(tuple(lo) if lo is not None else (0.0,) * 3,
+                        tuple(hi) if hi is not None else (1.0,) * 3)
+    ps = B.PointSet(d, x, dom)
+    w = np.asarray(w)
+    plan = B.Plan(ps, leaf, B.parse_kernel_spec(spec), sigma, m, c_table=c_table,
+                  nrhs=1 if w.ndim == 1 else w.shape[0])
+    return plan.execute(w), plan
+
+
+# Reduced sizes of every BASELINE config (same d, kernel, sigma, M, distribution).
+CASES = [
+    ("P1", 4096, 3),
+    ("P1b", 4096, 3),
+    ("P2p", 16384, 3),
+    ("P2", 4096, 2),
+    ("P3", 32768, 3),
+    ("P4", 65536, 6),
+    ("P5", 8192, 2),
+]
+
+
+@pytest.mark.parametrize("name,n,leaf", CASES)
+def test_mlfmm_matches_oracle(blfmm, oracle, name, n, leaf):
+    W = I.WORKLOADS[name]
+    x, w = W.make(n)
+    if w.ndim == 2:
+        w = w[:4]  # P5 batched: 4 rhs at reduced size
+    res, plan = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
+    ctab = blfmm.translation_coefficients(blfmm.parse_kernel_spec(W.kernel),
+                                          blfmm.make_quadrature(W.sigma, W.m, W.d)).c_vals
+    ov, ost, _ = oracle.mlfmm(x, w, W.kernel, W.sigma, W.m, leaf, c_table_in=ctab)
+    assert rel_l2(res.values, ov) <= TOL, rel_l2(res.values, ov)
+    assert res.stats.near_pairs == ost["near_pairs"]
+    assert res.stats.far_work == ost["far_work"]
+    assert abs(res.stats.max_imag_residual - ost["max_imag_residual"]) <= \
+        1e-8 * max(1.0, ost["max_imag_residual"])
+
+
+def test_golden_reference_fixtures(blfmm):
+    """Outputs of the reference itself (tests/golden, make_golden.py)."""
+    files = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+    assert files
+    for f in files:
+        g = np.load(f, allow_pickle=False)
+        res, _ = gpu_mlfmm(blfmm, g["x"], g["w"], str(g["spec"]), float(g["sigma"]),
+                           int(g["m"]), int(g["leaf"]))
+        assert rel_l2(res.values, g["values"]) <= TOL, (f, rel_l2(res.values, g["values"]))
+        assert res.stats.near_pairs == int(g["near_pairs"])
+        assert res.stats.far_work == int(g["far_work"])
+        if "direct" in g.files:
+            # independent O(N^2) GPU check of the same inputs
+            ps = blfmm.PointSet(g["x"].shape[1], g["x"])
+            dv = blfmm.direct_matvec(blfmm.parse_kernel_spec(str(g["spec"])), ps, g["w"]).values
+            assert rel_l2(dv, g["direct"]) <= 1e-14
+
+
+def test_band_capturing_regime_matches_direct(blfmm):
+    # P1b: sigma = spectrum_cutoff, FMM == direct to ~1e-15
+    W = I.WORKLOADS["P1b"]
+    x, w = W.make()
+    res, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, W.leaf)
+    dv = blfmm.direct_matvec(blfmm.parse_kernel_spec(W.kernel), blfmm.PointSet(2, x), w).values
+    assert rel_l2(res.values, dv) <= 1e-12
+
+
+@pytest.mark.parametrize("d,leaf,m,spec", [(2, 3, 16, "gaussian:c=16"), (3, 3, 6, "imq:c=0.1"),
+                                          (1, 5, 32, "imq:c=1")])
+def test_stage_expansions_match_oracle(blfmm, oracle, d, leaf, m, spec):
+    x = I.uniform_points(3000, d, 40 + d)
+    w = I.uniform_weights(3000, 50 + d)
+    ps = blfmm.PointSet(d, x)
+    plan = blfmm.Plan(ps, leaf, blfmm.parse_kernel_spec(spec), math.pi, m)
+    plan.set_keep_couple(True)
+    plan.execute(w)
+    for level in range(2, leaf + 1):
+        for kind in (0, 1, 2):
+            a = plan.expansions(level, kind)
+            b = oracle.expansions(x, w, spec, math.pi, m, leaf, level, kind)
+            scale = np.abs(b).max()
+            assert np.abs(a - b).max() <= 1e-12 * scale, (level, kind)
+
+
+def test_unit_source_coefficients_exact(blfmm):
+    # test_mlfmm.cpp:142-158: source at a leaf centre -> exactly 1+0i
+    ps = blfmm.PointSet(1, np.array([[0.375]]))
+    tree = blfmm.build_tree(ps, 2)
+    grids = blfmm.make_level_grids(blfmm.parse_kernel_spec("gaussian:c=1"), math.pi, 8, 1, 2)
+    ex = blfmm.upsweep(tree, grids, ps, np.array([1.0]))
+    assert np.all(ex[2][1] == 1.0 + 0.0j) and np.all(ex[2][0] == 0.0)
+    zero = blfmm.upsweep(tree, grids, ps, np.array([0.0]))
+    assert np.all(zero[2][1] == 0.0)
+
+
+def test_couple_scalar_hand_case(blfmm):
+    # test_mlfmm.cpp:191-220 analogue: only box 3 carries mass
+    x = np.array([[0.9]])
+    ps = blfmm.PointSet(1, x)
+    tree = blfmm.build_tree(ps, 2)
+    k = blfmm.parse_kernel_spec("gaussian:c=1")
+    grids = blfmm.make_level_grids(k, math.pi, 2, 1, 2)
+    mult = blfmm.upsweep(tree, grids, ps, np.array([1.5]))
+    loc = blfmm.couple(tree, grids, ps, np.array([1.5]))
+    c = grids.factors[2].c_vals
+    xi = grids.grids[2].nodes[:, 0]
+    # only box 3 is nonempty, so only its own local (IL 3 <- {0,1}: empty) is
+    # stored; boxes 0 and 1 have no points and are never targets.
+    assert np.all(loc[2][3] == 0.0)
+    assert np.allclose(mult[2][3], 1.5 * np.exp(1j * xi * (0.875 - 0.9)), rtol=1e-15, atol=1e-15)
+
+
+def test_three_point_direct_fixture(blfmm):
+    # test_fmm.cpp:37-49 through the GPU direct kernel
+    ps = blfmm.PointSet(1, np.array([[0.0], [0.5], [2.0]]))
+    r = blfmm.direct_matvec(blfmm.parse_kernel_spec("gaussian:c=1"), ps, np.array([1.0, 2.0, -1.0]))
+    np.testing.assert_allclose(r.values, [2.5392859272540756, 2.6734015585095405,
+                                          -0.77088591198753715], rtol=1e-15)
+    assert r.stats.near_pairs == 9
+
+
+def test_same_leaf_pair_reduces_to_direct(blfmm):
+    # test_fmm.cpp:119-129: far field empty -> bitwise the direct sum
+    ps = blfmm.PointSet(1, np.array([[0.1], [0.2]]))
+    tree = blfmm.build_tree(ps, 2)
+    k = blfmm.parse_kernel_spec("gaussian:c=1")
+    req = blfmm.SumRequest(k, math.pi, ps, np.array([1.0, 2.0]), 8)
+    fmm = blfmm.fmm_matvec_single(req, tree)
+    ref = blfmm.direct_matvec(k, ps, req.weights)
+    assert np.array_equal(fmm.values, ref.values)
+    assert fmm.stats.near_pairs == 4
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_telescoping_vs_single_level(blfmm, oracle, d):
+    # test_mlfmm.cpp:321-334 through the mirror API
+    n, leaf, m = 256, (4 if d == 1 else 3), (32 if d == 1 else 12)
+    x = I.generate_quasiuniform(n, d, 77, 0.4)
+    w = I.uniform_weights(n, 8)
+    k = blfmm.parse_kernel_spec("imq:c=1")
+    ps = blfmm.PointSet(d, x)
+    tree = blfmm.build_tree(ps, leaf)
+    grids = blfmm.make_level_grids(k, math.pi, m, d, leaf)
+    req = blfmm.SumRequest(k, math.pi, ps, w, m)
+    ml = blfmm.mlfmm_matvec(req, tree, grids)
+    sl, sst = oracle.single(x, w, "imq:c=1", math.pi, m, leaf)
+    assert np.abs(ml.values - sl).max() / np.abs(sl).max() < 1e-12
+    gs = blfmm.fmm_matvec_single(req, tree)
+    assert gs.stats.far_work == sst["far_work"] and gs.stats.near_pairs == sst["near_pairs"]
+
+
+def test_linearity(blfmm):
+    W = I.WORKLOADS["P3"]
+    x, w1 = W.make(20000)
+    w2 = I.uniform_weights(20000, 77)
+    ps = blfmm.PointSet(3, x)
+    plan = blfmm.Plan(ps, 4, blfmm.parse_kernel_spec(W.kernel), W.sigma, W.m)
+    a = plan.execute(w1).values
+    b = plan.execute(w2).values
+    c = plan.execute(0.37 * w1 + w2).values
+    assert np.abs(0.37 * a + b - c).max() <= 1e-12 * np.abs(c).max()
+
+
+def test_batched_rhs_equals_single_rhs(blfmm):
+    W = I.WORKLOADS["P5"]
+    x, w = W.make(4096)
+    w = w[:3]
+    ps = blfmm.PointSet(3, x)
+    k = blfmm.parse_kernel_spec(W.kernel)
+    pb = blfmm.Plan(ps, 2, k, W.sigma, 8, nrhs=3)
+    p1 = blfmm.Plan(ps, 2, k, W.sigma, 8, nrhs=1)
+    vb = pb.execute(w).values
+    for r in range(3):
+        v1 = p1.execute(w[r]).values
+        assert rel_l2(vb[r], v1) <= 1e-15
+
+
+def test_edge_cases(blfmm, oracle):
+    k = "imq:c=0.1"
+    # empty point set
+    res, plan = gpu_mlfmm(blfmm, np.zeros((0, 3)), np.zeros(0), k, math.pi, 4, 3)
+    assert res.values.shape == (0,) and res.stats.near_pairs == 0
+    # single point (only the self term phi(0) = 1/c)
+    res, _ = gpu_mlfmm(blfmm, np.array([[0.3, 0.4, 0.5]]), np.array([2.0]), k, math.pi, 4, 3)
+    assert abs(res.values[0] - 2.0 / 0.1) <= 1e-13 * 20
+    # boundary coordinates exactly 0 and 1 (clamped binning), duplicates,
+    # clustered points leaving most boxes empty, leaf level 2
+    rng = np.random.default_rng(3)
+    x = np.concatenate([rng.random((300, 3)) * 0.1, np.array([[0, 0, 0], [1, 1, 1], [1, 0, 1],
+                                                               [0.5, 0.5, 0.5], [0.5, 0.5, 0.5]])])
+    w = rng.uniform(-1, 1, x.shape[0])
+    for leaf in (2, 3, 5):
+        res, _ = gpu_mlfmm(blfmm, x, w, k, math.pi, 6, leaf)
+        ov, ost, _ = oracle.mlfmm(x, w, k, math.pi, 6, leaf)
+        assert rel_l2(res.values, ov) <= TOL and res.stats.near_pairs == ost["near_pairs"]
+    # a non-unit domain (read_points_csv-style tight box)
+    x2 = rng.random((500, 2)) * 3.0 - 1.0
+    lo, hi = x2.min(0) - 1e-9, x2.max(0) + 1e-9
+    w2 = rng.uniform(-1, 1, 500)
+    res, _ = gpu_mlfmm(blfmm, x2, w2, "mq:c=0.05", math.pi, 8, 3, lo=lo, hi=hi)
+    ov, _, _ = oracle.mlfmm(x2, w2, "mq:c=0.05", math.pi, 8, 3, lo=lo, hi=hi)
+    assert rel_l2(res.values, ov) <= TOL
+
+
+def test_validation_matches_reference_errors(blfmm):
+    ps = blfmm.PointSet(2, np.random.default_rng(0).random((64, 2)))
+    k = blfmm.parse_kernel_spec("imq:c=1")
+    tree = blfmm.build_tree(ps, 3)
+    grids = blfmm.make_level_grids(k, math.pi, 8, 2, 4)
+    with pytest.raises(blfmm.InvalidArgument):  # mlfmm.cpp:367-368
+        blfmm.mlfmm_matvec(blfmm.SumRequest(k, math.pi, ps, np.zeros(64), 8), tree, grids)
+    grids = blfmm.make_level_grids(k, math.pi, 8, 2, 3)
+    with pytest.raises(blfmm.InvalidArgument):  # weights length
+        blfmm.mlfmm_matvec(blfmm.SumRequest(k, math.pi, ps, np.zeros(63), 8), tree, grids)
+    with pytest.raises(blfmm.InvalidArgument):
+        blfmm.mlfmm_matvec(blfmm.SumRequest(k, math.pi, None, np.zeros(64), 8), tree, grids)
+    with pytest.raises(blfmm.DomainError):
+        blfmm.Plan(ps, 3, blfmm.parse_kernel_spec("tps:beta=2"), math.pi, 8)
+
+
+@pytest.mark.slow
+def test_full_size_p3_properties(blfmm):
+    """BASELINE config 3 at full size: linearity, permutation invariance, and
+    zero-frequency conservation (node M/2 of every multipole is sum lambda)."""
+    W = I.WORKLOADS["P3"]
+    x, w = W.make()
+    k = blfmm.parse_kernel_spec(W.kernel)
+    plan = blfmm.Plan(blfmm.PointSet(3, x), W.leaf, k, W.sigma, W.m)
+    v = plan.execute(w).values
+    w2 = I.uniform_weights(W.n, 4242)
+    v2 = plan.execute(w2).values
+    v3 = plan.execute(w - 0.5 * w2).values
+    assert np.abs(v - 0.5 * v2 - v3).max() <= 1e-11 * np.abs(v3).max()
+    perm = np.random.default_rng(1).permutation(W.n)
+    pp = blfmm.Plan(blfmm.PointSet(3, x[perm]), W.leaf, k, W.sigma, W.m)
+    vp = pp.execute(w[perm]).values
+    assert rel_l2(vp, v[perm]) <= 1e-13
+    m0 = (W.m // 2) * (W.m * W.m + W.m + 1)  # xi = (0,0,0)
+    plan.execute(w)
+    ex2 = plan.expansions(2, 0)
+    assert abs(ex2[:, m0].sum().real - w.sum()) <= 1e-10 * np.abs(w).sum()
