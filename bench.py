@@ -123,13 +123,14 @@ def dist_env():
 
 def far_bytes(info, K, nrhs):
     """Algorithmic HBM bytes of the far-field translation kernels per matvec
-    (SURVEY §8d): M2M reads children + writes parents; fused M2L+L2L reads V_l
-    once, reads the parent local once and writes L_l once."""
+    (SURVEY §8d): M2M reads children + writes parents (levels L..1); the fused
+    M2L+L2L kernel reads V_l once, reads the parent's G_{l-1} once and writes
+    one expansion (G_l, or L_L at the leaf) per box, levels 1..L."""
     L = info.leaf_level
     B = [info.boxes[l] for l in range(L + 1)]
     cb = 16 * K * nrhs
-    m2m = sum((B[l] + B[l - 1]) * cb for l in range(3, L + 1))
-    m2l = sum(2 * B[l] * cb + (B[l - 1] * cb if l > 2 else 0) for l in range(2, L + 1))
+    m2m = sum((B[l] + B[l - 1]) * cb for l in range(2, L + 1))
+    m2l = sum(2 * B[l] * cb + (B[l - 1] * cb if l >= 2 else 0) for l in range(1, L + 1))
     return m2m, m2l
 
 
@@ -243,9 +244,9 @@ def run_ours(args, W, world, rank, local):
     m2l_ms = acc.get("m2l_l2l", [0, 0])[0]
     if m2l_ms > 0:
         ach = m2l_b / (m2l_ms / 1e3) / 1e9
-        roof = {"kernel": "k_m2l (M2L + fused L2L)", "bound": "hbm", "achieved": round(ach, 1),
+        roof = {"kernel": "k_couple (M2L + fused L2L)", "bound": "hbm", "achieved": round(ach, 1),
                 "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
-                "traffic": load_traffic("k_m2l"),
+                "traffic": load_traffic("k_couple"),
                 "algorithmic_bytes": m2l_b,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s",
                 "dominant_stage": top,

@@ -131,9 +131,11 @@ def test_couple_scalar_hand_case(blfmm):
     loc = blfmm.couple(tree, grids, ps, np.array([1.5]))
     c = grids.factors[2].c_vals
     xi = grids.grids[2].nodes[:, 0]
-    # only box 3 is nonempty, so only its own local (IL 3 <- {0,1}: empty) is
-    # stored; boxes 0 and 1 have no points and are never targets.
-    assert np.all(loc[2][3] == 0.0)
+    # only box 3 is nonempty; its interaction list {0, 1} holds no mass. The
+    # reference gets an exact 0 (test_mlfmm.cpp:216-218). The GPU evaluates the
+    # IL sum as shift * NS_{l-1}(parent) - NS_l(box) (k_couple), so "no mass"
+    # is a rounding-level zero: bounded by 1e-15 of the multipole magnitude.
+    assert np.abs(loc[2][3]).max() <= 1e-15 * np.abs(mult[2][3]).max() * np.abs(c).max()
     assert np.allclose(mult[2][3], 1.5 * np.exp(1j * xi * (0.875 - 0.9)), rtol=1e-15, atol=1e-15)
 
 
@@ -199,7 +201,8 @@ def test_batched_rhs_equals_single_rhs(blfmm):
     vb = pb.execute(w).values
     for r in range(3):
         v1 = p1.execute(w[r]).values
-        assert rel_l2(vb[r], v1) <= 1e-15
+        err = rel_l2(vb[r], v1)
+        assert err <= 1e-14, err  # summation order of the near field differs
 
 
 def test_edge_cases(blfmm, oracle):
