@@ -159,6 +159,17 @@ int blfmm_set_keep_couple(blfmm_plan* plan, int enable);
 int blfmm_set_profiling(blfmm_plan* plan, int enable);
 int blfmm_get_stage_times(const blfmm_plan* plan, blfmm_stage_times* t);
 
+/* Morton-range sharding (multi-GPU). A plan created with world > 1 builds
+ * the same tree on every rank, runs the full upsweep, and evaluates the
+ * downsweep and near field only for its own contiguous range of leaves
+ * (equal estimated cost). blfmm_execute writes the owned targets and zeros
+ * elsewhere, so an all-reduce(sum) of the outputs of all ranks is u.
+ * blfmm_partition is the host-side splitter (bounds[0..world]);
+ * blfmm_plan_owned_points lists the owned targets' caller indices
+ * (info.owned_end - info.owned_begin entries). */
+int blfmm_partition(const double* cost, long long n, int world, long long* bounds);
+int blfmm_plan_owned_points(const blfmm_plan* plan, long long* idx);
+
 /* Independent O(N^2) check (direct_matvec, fmm.cpp:30-75): values for
  * n_targets target indices (NULL = all n) into HOST out. */
 int blfmm_direct(int d, long long n, const double* coords, int kernel_type,

@@ -80,6 +80,9 @@ EXPORTS = {
     "blfmm_set_keep_couple": (ct.c_int, [ct.c_void_p, ct.c_int]),
     "blfmm_set_profiling": (ct.c_int, [ct.c_void_p, ct.c_int]),
     "blfmm_get_stage_times": (ct.c_int, [ct.c_void_p, ct.POINTER(StageTimes)]),
+    "blfmm_partition": (ct.c_int, [ct.POINTER(ct.c_double), ct.c_longlong, ct.c_int,
+                                   ct.POINTER(ct.c_longlong)]),
+    "blfmm_plan_owned_points": (ct.c_int, [ct.c_void_p, ct.POINTER(ct.c_longlong)]),
     "blfmm_direct": (ct.c_int, [ct.c_int, ct.c_longlong, ct.POINTER(ct.c_double), ct.c_int,
                                 ct.c_double, ct.POINTER(ct.c_double), ct.c_longlong,
                                 ct.POINTER(ct.c_longlong), ct.POINTER(ct.c_double), ct.c_int]),

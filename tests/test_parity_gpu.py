@@ -269,3 +269,29 @@ def test_full_size_p3_properties(blfmm):
     plan.execute(w)
     ex2 = plan.expansions(2, 0)
     assert abs(ex2[:, m0].sum().real - w.sum()) <= 1e-10 * np.abs(w).sum()
+
+
+@pytest.mark.parametrize("name,n,leaf", [("P3", 60000, 4), ("P4", 50000, 5), ("P1", 4096, 3)])
+def test_sharded_plans_assemble_to_full(blfmm, name, n, leaf):
+    """Morton-range sharding: the owned outputs of world plans (one per rank,
+    here all on one GPU, no collective) sum to the single-plan matvec exactly,
+    and the owned near-pair counts add up."""
+    W = I.WORKLOADS[name]
+    x, w = W.make(n)
+    k = blfmm.parse_kernel_spec(W.kernel)
+    ps = blfmm.PointSet(W.d, x)
+    full = blfmm.Plan(ps, leaf, k, W.sigma, W.m).execute(w)
+    for world in (2, 3, 8):
+        acc = np.zeros_like(full.values)
+        pairs = 0
+        owned = []
+        for rank in range(world):
+            pl = blfmm.Plan(ps, leaf, k, W.sigma, W.m, rank=rank, world=world)
+            r = pl.execute(w)
+            acc += r.values
+            pairs += r.stats.near_pairs
+            inf = pl.info()
+            owned.append(inf.owned_end - inf.owned_begin)
+        assert np.array_equal(acc, full.values), world
+        assert pairs == full.stats.near_pairs
+        assert sum(owned) == n
