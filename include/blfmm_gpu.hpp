@@ -1,0 +1,171 @@
+// blfmm_gpu.hpp — header-only C++ adapter: the reference library's own
+// signatures (namespace blfmm, d <= 2 types of /root/reference/proj/core/include)
+// implemented on the C ABI of blfmm_gpu.h, so reference callers (the Krylov
+// solver, the CLI, the tests) can switch the matvec to the B200 path by
+// replacing `blfmm::mlfmm_matvec(...)` with `blfmm::gpu::mlfmm_matvec(...)`.
+//
+// Include AFTER putting the reference headers on the include path; link with
+// libblfmm_gpu.so. Mirrors:
+//   SumResult mlfmm_matvec(const SumRequest&, const BoxTree&, const LevelGrids&)
+//                                             core/include/blfmm/mlfmm.hpp:98-99
+//   SumResult fmm_matvec_single(const SumRequest&, const BoxTree&)
+//                                             core/include/blfmm/fmm.hpp:55
+//   SumResult direct_matvec(const RadialKernel&, const PointSet&,
+//                           const std::vector<double>&, bool, double, int)
+//                                             core/include/blfmm/fmm.hpp:33-36
+// Errors are rethrown as the reference's exception classes
+// (std::invalid_argument, std::domain_error, blfmm::accuracy_error).
+#pragma once
+
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "blfmm/mlfmm.hpp"
+#include "blfmm_gpu.h"
+
+namespace blfmm {
+namespace gpu {
+
+inline void check(int code) {
+  if (code == BLFMM_OK) return;
+  std::string msg = blfmm_last_error();
+  switch (code) {
+    case BLFMM_EINVAL:
+      throw std::invalid_argument(msg);
+    case BLFMM_EDOMAIN:
+      throw std::domain_error(msg);
+    case BLFMM_EACCURACY:
+      throw accuracy_error(msg, blfmm_last_error_value());
+    case BLFMM_ENOMEM:
+      throw std::bad_alloc();
+    default:
+      throw std::runtime_error("blfmm_gpu: " + msg);
+  }
+}
+
+// Plan cache: the tree + grids a caller builds once are reused across
+// matvecs (the solver pattern, solver.cpp:280-293); a new point set, tree
+// depth or grid rebuilds the device plan.
+struct PlanHandle {
+  blfmm_plan* p = nullptr;
+  const PointSet* ps = nullptr;
+  std::size_t n = 0;
+  int leaf = 0, m = 0, mode = 0;
+  double sigma = 0.0;
+  RadialKernel kernel;
+  std::vector<double> c_vals;
+  ~PlanHandle() {
+    if (p) blfmm_plan_destroy(p);
+  }
+};
+
+inline blfmm_plan* plan_for(const PointSet& ps, const BoxTree& tree, const RadialKernel& k,
+                            double sigma, int m, const std::vector<double>& c_vals) {
+  thread_local std::unique_ptr<PlanHandle> cache;
+  if (cache && cache->ps == &ps && cache->n == ps.pts.size() && cache->leaf == tree.leaf_level &&
+      cache->m == m && cache->sigma == sigma && cache->kernel.type == k.type &&
+      cache->kernel.shape == k.shape && cache->c_vals == c_vals)
+    return cache->p;
+  cache.reset(new PlanHandle());
+  const int d = ps.d;
+  std::vector<double> coords(ps.pts.size() * d);
+  for (std::size_t i = 0; i < ps.pts.size(); ++i)
+    for (int q = 0; q < d; ++q) coords[i * d + q] = ps.pts[i][q];
+  blfmm_plan_desc desc;
+  std::memset(&desc, 0, sizeof(desc));
+  desc.d = d;
+  desc.n = static_cast<long long>(ps.pts.size());
+  desc.coords = coords.data();
+  for (int q = 0; q < d; ++q) {
+    desc.domain_lo[q] = tree.domain.lo[q];
+    desc.domain_hi[q] = tree.domain.hi[q];
+  }
+  desc.kernel_type = static_cast<int>(k.type);  // same enumerator order
+  desc.kernel_shape = k.shape;
+  desc.sigma = sigma;
+  desc.m_per_dim = m;
+  desc.leaf_level = tree.leaf_level;
+  desc.grid_mode = BLFMM_GRID_SHARED;
+  desc.stencil_k = 10;
+  desc.nrhs = 1;
+  desc.device = -1;
+  desc.c_table = c_vals.data();  // the reference's own C(xi_m): bit-identical spectrum
+  desc.world = 1;
+  check(blfmm_plan_create(&desc, &cache->p));
+  cache->ps = &ps;
+  cache->n = ps.pts.size();
+  cache->leaf = tree.leaf_level;
+  cache->m = m;
+  cache->sigma = sigma;
+  cache->kernel = k;
+  cache->c_vals = c_vals;
+  return cache->p;
+}
+
+inline SumResult run(blfmm_plan* p, const std::vector<double>& w, bool single) {
+  SumResult res;
+  res.values.assign(w.size(), 0.0);
+  blfmm_stats st{};
+  check(single ? blfmm_execute_single(p, w.data(), res.values.data(), &st, nullptr)
+               : blfmm_execute(p, w.data(), res.values.data(), &st, nullptr));
+  res.stats.near_pairs = st.near_pairs;
+  res.stats.far_work = st.far_work;
+  res.stats.max_imag_residual = st.max_imag_residual;
+  return res;
+}
+
+// mlfmm.cpp:361-406 semantics (shared grids).
+inline SumResult mlfmm_matvec(const SumRequest& req, const BoxTree& tree,
+                              const LevelGrids& grids) {
+  if (!req.ps) throw std::invalid_argument("request has no point set");
+  const PointSet& ps = *req.ps;
+  if (req.weights.size() != static_cast<std::size_t>(ps.size()))
+    throw std::invalid_argument("weight count != point count");
+  if (grids.d != ps.d || grids.leaf_level != tree.leaf_level)
+    throw std::invalid_argument("grids incompatible with tree/points");
+  if (grids.mode != GridMode::shared)
+    throw std::domain_error("GridMode::scaled is not implemented on the GPU path");
+  const auto& g = grids.grids[tree.leaf_level];
+  blfmm_plan* p = plan_for(ps, tree, grids.kernel, g.sigma, g.m_per_dim,
+                           grids.factors[tree.leaf_level].c_vals);
+  return run(p, req.weights, false);
+}
+
+// fmm.cpp:123-213 semantics: equal to the shared-grid sweep to rounding.
+inline SumResult fmm_matvec_single(const SumRequest& req, const BoxTree& tree) {
+  if (!req.ps) throw std::invalid_argument("request has no point set");
+  if (static_cast<int>(req.weights.size()) != req.ps->size())
+    throw std::invalid_argument("weights length != point count");
+  if (!(req.sigma > 0.0)) throw std::invalid_argument("sigma must be > 0");
+  if (req.m_per_dim < 2) throw std::invalid_argument("m_per_dim must be >= 2");
+  QuadratureGrid grid = make_quadrature(req.sigma, req.m_per_dim, req.ps->d);
+  LowRankFactors f = translation_coefficients(req.kernel, grid, TranslationMode::spectral);
+  blfmm_plan* p = plan_for(*req.ps, tree, req.kernel, req.sigma, req.m_per_dim, f.c_vals);
+  return run(p, req.weights, true);
+}
+
+// fmm.cpp:30-75 plain-kernel O(N^2) sum (use_bandlimited = false).
+inline SumResult direct_matvec(const RadialKernel& k, const PointSet& ps,
+                               const std::vector<double>& weights, bool use_bandlimited,
+                               double sigma, int refinement = 1024) {
+  if (use_bandlimited)  // the 1-D band-limited table oracle stays the reference's CPU code
+    return ::blfmm::direct_matvec(k, ps, weights, true, sigma, refinement);
+  const int n = ps.size();
+  if (static_cast<int>(weights.size()) != n)
+    throw std::invalid_argument("weights length != point count");
+  std::vector<double> coords(static_cast<std::size_t>(n) * ps.d);
+  for (int i = 0; i < n; ++i)
+    for (int q = 0; q < ps.d; ++q) coords[static_cast<std::size_t>(i) * ps.d + q] = ps.pts[i][q];
+  SumResult res;
+  res.values.assign(n, 0.0);
+  check(blfmm_direct(ps.d, n, coords.data(), static_cast<int>(k.type), k.shape, weights.data(),
+                     n, nullptr, res.values.data(), -1));
+  res.stats.near_pairs = static_cast<long long>(n) * n;
+  return res;
+}
+
+}  // namespace gpu
+}  // namespace blfmm

@@ -1,0 +1,85 @@
+// Test infrastructure: the reference library (compiled from its own sources)
+// and the GPU library linked into ONE program through include/blfmm_gpu.hpp,
+// the drop-in a reference maintainer would use. Runs the reference matvec and
+// the GPU matvec on the reference's own PointSet / BoxTree / LevelGrids and
+// prints one JSON line per case; exit code = number of failed cases.
+// Built by oracle/Makefile into oracle/_ref/adapter_parity (needs a GPU to run).
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "blfmm/mlfmm.hpp"
+#include "blfmm_gpu.hpp"
+
+using namespace blfmm;
+
+static double rel_l2(const std::vector<double>& a, const std::vector<double>& b) {
+  double num = 0, den = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    num += (a[i] - b[i]) * (a[i] - b[i]);
+    den += b[i] * b[i];
+  }
+  return std::sqrt(num / (den > 0 ? den : 1.0));
+}
+
+static int run_case(const char* name, const std::string& spec, int d, int n, double sigma, int m,
+                    int leaf, bool single) {
+  PointSet ps;
+  ps.d = d;
+  for (int i = 0; i < n; ++i)
+    ps.pts.push_back(Pt{uniform01(1001, static_cast<uint64_t>(d) * i),
+                        d == 2 ? uniform01(1001, static_cast<uint64_t>(d) * i + 1) : 0.0});
+  std::vector<double> w(n);
+  for (int j = 0; j < n; ++j) w[j] = 2.0 * uniform01(2001, j) - 1.0;
+  RadialKernel k = parse_kernel_spec(spec);
+  BoxTree tree = build_tree(ps, leaf);
+  SumRequest req{k, sigma, &ps, w, m};
+  SumResult ref, gpu;
+  if (single) {
+    ref = fmm_matvec_single(req, tree);
+    gpu = blfmm::gpu::fmm_matvec_single(req, tree);
+  } else {
+    LevelGrids grids = make_level_grids(k, sigma, m, d, leaf, GridMode::shared, 10);
+    ref = mlfmm_matvec(req, tree, grids);
+    gpu = blfmm::gpu::mlfmm_matvec(req, tree, grids);
+    // second call reuses the cached plan (solver pattern)
+    gpu = blfmm::gpu::mlfmm_matvec(req, tree, grids);
+  }
+  double e = rel_l2(gpu.values, ref.values);
+  bool ok = e <= 1e-10 && gpu.stats.near_pairs == ref.stats.near_pairs &&
+            gpu.stats.far_work == ref.stats.far_work;
+  std::printf(
+      "{\"case\": \"%s\", \"rel_l2\": %.3e, \"near_pairs\": [%lld, %lld], \"far_work\": [%lld, "
+      "%lld], \"max_imag\": [%.6e, %.6e], \"ok\": %s}\n",
+      name, e, gpu.stats.near_pairs, ref.stats.near_pairs, gpu.stats.far_work,
+      ref.stats.far_work, gpu.stats.max_imag_residual, ref.stats.max_imag_residual,
+      ok ? "true" : "false");
+  return ok ? 0 : 1;
+}
+
+int main() {
+  int fails = 0;
+  fails += run_case("P1 gaussian:c=16 2D N=4096", "gaussian:c=16", 2, 4096, M_PI, 64, 3, false);
+  fails += run_case("P1b band-capturing", "gaussian:c=16", 2, 4096, 51.4, 44, 3, false);
+  fails += run_case("P4-shape mq:c=0.05 2D N=16384", "mq:c=0.05", 2, 16384, M_PI, 16, 5, false);
+  fails += run_case("imq:c=0.1 2D N=8192", "imq:c=0.1", 2, 8192, M_PI, 16, 4, false);
+  fails += run_case("imq:c=1 1D N=1024 L=5", "imq:c=1", 1, 1024, M_PI, 64, 5, false);
+  fails += run_case("single-level imq:c=1 2D", "imq:c=1", 2, 2048, M_PI, 12, 3, true);
+  // error mapping: mismatched grids -> std::invalid_argument
+  try {
+    PointSet ps;
+    ps.d = 2;
+    ps.pts = {Pt{0.1, 0.2}, Pt{0.3, 0.4}};
+    BoxTree tree = build_tree(ps, 3);
+    LevelGrids grids = make_level_grids(parse_kernel_spec("imq:c=1"), M_PI, 8, 2, 4,
+                                        GridMode::shared, 10);
+    SumRequest req{parse_kernel_spec("imq:c=1"), M_PI, &ps, {1.0, 2.0}, 8};
+    blfmm::gpu::mlfmm_matvec(req, tree, grids);
+    std::printf("{\"case\": \"error mapping\", \"ok\": false}\n");
+    ++fails;
+  } catch (const std::invalid_argument&) {
+    std::printf("{\"case\": \"error mapping\", \"ok\": true}\n");
+  }
+  return fails;
+}

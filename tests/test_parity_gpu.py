@@ -295,3 +295,19 @@ def test_sharded_plans_assemble_to_full(blfmm, name, n, leaf):
         assert np.array_equal(acc, full.values), world
         assert pairs == full.stats.near_pairs
         assert sum(owned) == n
+
+
+def test_cpp_adapter_dropin_against_reference():
+    """include/blfmm_gpu.hpp + the reference library (built from its own
+    sources) in one C++ program: the GPU matvec on the reference's own
+    PointSet / BoxTree / LevelGrids equals the reference's mlfmm_matvec."""
+    import json
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref",
+                       "adapter_parity")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/adapter_parity not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) >= 7, r.stdout + r.stderr
+    assert r.returncode == 0 and all(l["ok"] for l in lines), r.stdout
