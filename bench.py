@@ -61,7 +61,7 @@ def fp64_peak():
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -86,6 +86,11 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def mark(self, which):
+        """Wall-clock bounds of the timed region (samples outside are dropped)."""
+        import datetime
+        setattr(self, which, datetime.datetime.now())
+
     def __exit__(self, *a):
         if self.proc:
             self.proc.terminate()
@@ -95,18 +100,24 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        import datetime
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        t0 = getattr(self, "t0", None)
+        t1 = getattr(self, "t1", None)
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
+            if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
+                if t0 and t1 and not (t0 - datetime.timedelta(milliseconds=150) <= ts <= t1):
+                    continue
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[4:8]):
+            for nm, v in zip(names, parts[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         under = [s for s in sm if mx and s > 0.5 * mx] or sm
@@ -180,11 +191,19 @@ def run_ours(args, W, world, rank, local):
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        # keep the GPU busy while nvidia-smi starts sampling, then time
+        t_start = time.perf_counter()
+        while time.perf_counter() - t_start < 0.5:
+            step()
+            torch.cuda.synchronize(dev)
+        barrier()
+        clk.mark("t0")
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize(dev)
+        clk.mark("t1")
     barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
@@ -310,12 +329,13 @@ def ct_stream(stream):
 
 
 def load_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu --set full
-    capture summary (profiles/ncu_summary.json), or None."""
+    """DRAM bytes (read + write) of `kernel` per matvec (all its launches of
+    one step, matching `achieved`), from the committed ncu capture
+    profiles/r01_ncu_step_dram.json, or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_step_dram.json")) as f:
             s = json.load(f)
-        return s.get(kernel, {}).get("dram_bytes_per_launch")
+        return s["kernels"][kernel]["dram_bytes_total"]
     except Exception:
         return None
 
@@ -372,7 +392,7 @@ def run_reference(args, W):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="P3", choices=sorted(I.WORKLOADS))
