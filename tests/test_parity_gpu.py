@@ -311,3 +311,20 @@ def test_cpp_adapter_dropin_against_reference():
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) >= 7, r.stdout + r.stderr
     assert r.returncode == 0 and all(l["ok"] for l in lines), r.stdout
+
+
+@pytest.mark.parametrize("nr", [16, 32])
+def test_batched_rhs_near_field_path(blfmm, oracle, nr):
+    """nrhs multiple of 16 takes the batched near-field kernel (point-major
+    weights, one phi per pair for 16 right-hand sides)."""
+    W = I.WORKLOADS["P5"]
+    x, w = W.make(4096)
+    w = np.ascontiguousarray(w[:nr])
+    ps = blfmm.PointSet(3, x)
+    k = blfmm.parse_kernel_spec(W.kernel)
+    vb = blfmm.Plan(ps, 3, k, W.sigma, 8, nrhs=nr).execute(w).values
+    ov, _, _ = oracle.mlfmm(x, w[[0, nr - 1]], W.kernel, W.sigma, 8, 3)
+    assert rel_l2(vb[0], ov[0]) <= TOL and rel_l2(vb[nr - 1], ov[1]) <= TOL
+    p1 = blfmm.Plan(ps, 3, k, W.sigma, 8, nrhs=1)
+    for r in (0, 7, nr - 1):
+        assert rel_l2(vb[r], p1.execute(w[r]).values) <= 1e-14
