@@ -136,8 +136,9 @@ int blfmm_plan_get_info(const blfmm_plan* plan, blfmm_plan_info* info);
 int blfmm_execute(blfmm_plan* plan, const double* lambda, double* out,
                   blfmm_stats* stats, void* stream);
 
-/* Same with DEVICE buffers (no copies, no synchronisation; stats may be NULL
- * to avoid the D2H read of max_imag_residual). */
+/* Same with DEVICE buffers (no copies, no host synchronisation; stats may be
+ * NULL to avoid the D2H read of max_imag_residual). The work is ordered after
+ * and before `stream` (NULL = the legacy default stream). */
 int blfmm_execute_device(blfmm_plan* plan, const double* d_lambda,
                          double* d_out, blfmm_stats* stats, void* stream);
 

@@ -1,0 +1,225 @@
+"""Krylov interpolation solve on the GPU matvec (first "next" row).
+
+Mirrors ``solve_interpolation`` (/root/reference/proj/core/src/solver.cpp:243-300)
+and its Krylov loops ``run_cg`` (43-88) and ``run_gmres`` (90-203): CG when the
+kernel is positive definite, restarted GMRES(300) with Givens rotations
+otherwise; the same backend rules (dense / single-level FMM / multilevel FMM,
+sigma <= 0 -> pi, m <= 0 -> choose_truncation(N), leaf level from N), the same
+stopping tests and the same errors (invalid_argument, accuracy_error with the
+best residual). The plan (tree, grids, C table, expansion buffers) is built
+once and reused by every iteration, and all Krylov vectors stay on the device.
+"""
+from __future__ import annotations
+
+import enum
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .api import (AccuracyError, InvalidArgument, KernelType, Plan, PointSet, RadialKernel,
+                  choose_truncation, direct_matvec)
+
+
+class Backend(enum.IntEnum):
+    dense = 0
+    single_fmm = 1
+    mlfmm = 2
+
+
+@dataclass
+class InterpolationProblem:
+    kernel: RadialKernel
+    ps: PointSet | None = None
+    rhs: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    backend: Backend = Backend.dense
+    tol: float = 1e-10
+    max_iter: int = 2000
+    sigma: float = 0.0
+    m_per_dim: int = 0
+    leaf_level: int = 0
+
+
+@dataclass
+class SolveStats:
+    iterations: int = 0
+    residual: float = 0.0
+    matvecs: int = 0
+    method: str = ""
+    converged: bool = False
+
+
+def positive_definite(k: RadialKernel) -> bool:
+    """kernels.cpp:334-337 (Gaussian, IMQ, Wendland)."""
+    return k.type in (KernelType.Gaussian, KernelType.IMQ, KernelType.WendlandC2,
+                      KernelType.Wendland31)
+
+
+def run_cg(apply, b, tol: float, max_iter: int):
+    """solver.cpp:43-88 on torch tensors (any device)."""
+    import torch
+    stats = SolveStats(method="cg")
+    x = torch.zeros_like(b)
+    bnorm = torch.linalg.vector_norm(b).item()
+    if bnorm == 0.0:
+        stats.converged = True
+        return x, stats
+    r = b.clone()
+    p = b.clone()
+    rr = torch.dot(r, r).item()
+    best = math.sqrt(rr) / bnorm
+    for it in range(max_iter):
+        ap = apply(p)
+        stats.matvecs += 1
+        pap = torch.dot(p, ap).item()
+        if pap <= 0.0:  # not PD to working precision
+            break
+        alpha = rr / pap
+        x.add_(p, alpha=alpha)
+        r.sub_(ap, alpha=alpha)
+        rr_new = torch.dot(r, r).item()
+        stats.iterations = it + 1
+        rel = math.sqrt(rr_new) / bnorm
+        best = min(best, rel)
+        if rel <= tol:
+            stats.residual = rel
+            stats.converged = True
+            return x, stats
+        beta = rr_new / rr
+        rr = rr_new
+        p.mul_(beta).add_(r)
+    stats.residual = best
+    raise AccuracyError("cg did not reach tolerance", best)
+
+
+def run_gmres(apply, b, tol: float, max_iter: int):
+    """solver.cpp:90-203: restarted GMRES (restart 300), Givens rotations."""
+    import torch
+    stats = SolveStats(method="gmres")
+    n = b.shape[0]
+    x = torch.zeros_like(b)
+    bnorm = torch.linalg.vector_norm(b).item()
+    if bnorm == 0.0:
+        stats.converged = True
+        return x, stats
+    restart = min(max_iter, 300)
+    best = math.inf
+    total_it = 0
+    while total_it < max_iter:
+        if total_it == 0:
+            r = b.clone()
+        else:
+            r = b - apply(x)
+            stats.matvecs += 1
+        beta = torch.linalg.vector_norm(r).item()
+        if beta / bnorm <= tol:
+            stats.residual = beta / bnorm
+            stats.converged = True
+            return x, stats
+        m = min(restart, max_iter - total_it)
+        V = torch.zeros((m + 1, n), dtype=b.dtype, device=b.device)
+        V[0] = r / beta
+        H = np.zeros((m + 1, m + 1))  # H[k][j] = column k, row j (as the reference)
+        cs, sn, g = [], [], [beta]
+        k = 0
+        while k < m:
+            w = apply(V[k])
+            stats.matvecs += 1
+            # modified Gram-Schmidt, one projection at a time (as the reference)
+            for j in range(k + 1):
+                d = torch.dot(w, V[j])
+                H[k][j] = d.item()
+                w = w - d * V[j]
+            wn = torch.linalg.vector_norm(w).item()
+            H[k][k + 1] = wn
+            breakdown = wn < 1e-14 * beta
+            if not breakdown:
+                V[k + 1] = w / wn
+            for j in range(k):
+                t = cs[j] * H[k][j] + sn[j] * H[k][j + 1]
+                H[k][j + 1] = -sn[j] * H[k][j] + cs[j] * H[k][j + 1]
+                H[k][j] = t
+            denom = math.hypot(H[k][k], H[k][k + 1])
+            cs.append(H[k][k] / denom)
+            sn.append(H[k][k + 1] / denom)
+            H[k][k] = denom
+            H[k][k + 1] = 0.0
+            g.append(-sn[k] * g[k])
+            g[k] = cs[k] * g[k]
+            total_it += 1
+            stats.iterations = total_it
+            rel = abs(g[k + 1]) / bnorm
+            best = min(best, rel)
+            k += 1
+            if rel <= tol or breakdown:
+                break
+        y = np.zeros(k)
+        for j in range(k - 1, -1, -1):
+            s = g[j]
+            for l in range(j + 1, k):
+                s -= H[l][j] * y[l]
+            y[j] = s / H[j][j]
+        x = x + torch.mv(V[:k].T, torch.as_tensor(y, dtype=b.dtype, device=b.device))
+        res = (torch.linalg.vector_norm(b - apply(x)).item()) / bnorm
+        stats.matvecs += 1
+        best = min(best, res)
+        if res <= tol:
+            stats.residual = res
+            stats.converged = True
+            return x, stats
+    stats.residual = best
+    raise AccuracyError("gmres did not reach tolerance", best)
+
+
+def _lround(v: float) -> int:
+    """std::lround: half away from zero (Python's round() is half-to-even)."""
+    return int(math.floor(v + 0.5)) if v >= 0 else -int(math.floor(-v + 0.5))
+
+
+def _device_apply(plan: Plan):
+    import ctypes as ct
+
+    import torch
+    stream = torch.cuda.current_stream()
+    sp = ct.c_void_p(stream.cuda_stream)
+
+    def apply(x):
+        x = x.contiguous()
+        out = torch.empty_like(x)
+        plan.execute_device(x.data_ptr(), out.data_ptr(), stream=sp)
+        return out
+    return apply
+
+
+def solve_interpolation(prob: InterpolationProblem):
+    """solver.cpp:243-300. Returns (lambda [numpy], SolveStats)."""
+    import torch
+    if prob.ps is None:
+        raise InvalidArgument("problem has no point set")
+    ps = prob.ps
+    n = ps.size()
+    rhs = np.ascontiguousarray(prob.rhs, dtype=np.float64)
+    if rhs.shape != (n,):
+        raise InvalidArgument("rhs length != point count")
+    if not prob.tol > 0.0:
+        raise InvalidArgument("tol must be positive")
+    sigma = prob.sigma if prob.sigma > 0.0 else math.pi
+    m = prob.m_per_dim if prob.m_per_dim > 0 else choose_truncation(n)
+    dev = torch.device("cuda")
+    if prob.backend == Backend.dense:
+        def apply(x):
+            xv = x.detach().cpu().numpy()
+            return torch.from_numpy(direct_matvec(prob.kernel, ps, xv).values).to(dev)
+    elif prob.backend == Backend.single_fmm:
+        level = max(2, _lround(math.log2(math.sqrt(float(n)))))
+        level = prob.leaf_level if prob.leaf_level > 0 else level
+        apply = _device_apply(Plan(ps, level, prob.kernel, sigma, m))
+    else:
+        level = max(3, _lround(math.log2(float(n) / 32.0)))
+        if prob.leaf_level > 0:
+            level = prob.leaf_level
+        apply = _device_apply(Plan(ps, level, prob.kernel, sigma, m))
+    b = torch.from_numpy(rhs).to(dev)
+    runner = run_cg if positive_definite(prob.kernel) else run_gmres
+    x, stats = runner(apply, b, prob.tol, prob.max_iter)
+    return x.cpu().numpy(), stats

@@ -1,0 +1,71 @@
+"""Krylov caller (solver.cpp:43-300 semantics): CG / restarted GMRES on the
+CPU with a dense operator, and on the GPU through the FMM plan."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1606_07652_b200 import inputs as I
+from paper_1606_07652_b200 import solver as S
+
+
+def test_cg_gmres_dense_cpu():
+    rng = np.random.default_rng(0)
+    n = 120
+    q = rng.standard_normal((n, n))
+    spd = q @ q.T + n * np.eye(n)
+    ns = spd + 5.0 * np.triu(rng.standard_normal((n, n)), 1)
+    b = rng.standard_normal(n)
+    for A, run in ((spd, S.run_cg), (ns, S.run_gmres)):
+        At = torch.from_numpy(A)
+        x, st = run(lambda v: At @ v, torch.from_numpy(b), 1e-12, 500)
+        assert st.converged and st.residual <= 1e-12
+        np.testing.assert_allclose(x.numpy(), np.linalg.solve(A, b), rtol=1e-9, atol=1e-10)
+    # zero rhs, accuracy_error with the best residual
+    x, st = S.run_cg(lambda v: v, torch.zeros(4, dtype=torch.float64), 1e-10, 10)
+    assert st.converged and float(x.abs().max()) == 0.0
+    At = torch.from_numpy(ns)
+    with pytest.raises(S.AccuracyError) as e:
+        S.run_gmres(lambda v: At @ v, torch.from_numpy(b), 1e-14, 3)
+    assert e.value.achieved > 1e-14
+
+
+@pytest.mark.gpu
+def test_backends_agree_band_capturing(blfmm):
+    # test_solver.cpp:209-242: dense, single-level and multilevel backends
+    # solve the same operator when the band captures the spectrum
+    x = I.generate_quasiuniform(512, 1, 300, 0.4, lo=(0.0, 0.0), hi=(32.0, 1.0))
+    ps = blfmm.PointSet(1, x, blfmm.BoundingBox((0.0, 0.0, 0.0), (32.0, 1.0, 1.0)))
+    rhs = np.sin(math.pi * x[:, 0] / 32.0) + 0.5 * np.cos(3.0 * math.pi * x[:, 0] / 32.0)
+    k = blfmm.parse_kernel_spec("gaussian:c=256")
+    out = {}
+    for be in S.Backend:
+        prob = S.InterpolationProblem(k, ps, rhs, be, tol=1e-12, sigma=203.0, m_per_dim=2112)
+        lam, st = S.solve_interpolation(prob)
+        assert st.method == "cg" and st.converged
+        out[be] = lam
+    assert np.abs(out[S.Backend.dense] - out[S.Backend.single_fmm]).max() < 1e-8
+    assert np.abs(out[S.Backend.dense] - out[S.Backend.mlfmm]).max() < 1e-8
+    u = blfmm.direct_matvec(k, ps, out[S.Backend.mlfmm]).values
+    assert np.abs(u - rhs).max() <= 10 * 1e-12 * np.abs(rhs).max()
+
+
+@pytest.mark.gpu
+def test_gmres_on_mq_and_validation(blfmm):
+    # MQ (conditionally positive definite) -> GMRES; cond(A) ~ 1e7 here
+    xs = I.uniform_points(400, 2, 5)
+    ps = blfmm.PointSet(2, xs)
+    k = blfmm.parse_kernel_spec("mq:c=0.02")
+    rhs = np.cos(3 * xs[:, 0]) * xs[:, 1]
+    lam, st = S.solve_interpolation(S.InterpolationProblem(k, ps, rhs, S.Backend.dense,
+                                                           tol=1e-10))
+    assert st.method == "gmres" and st.converged and st.residual <= 1e-10
+    u = blfmm.direct_matvec(k, ps, lam).values
+    assert np.linalg.norm(u - rhs) <= 1e-9 * np.linalg.norm(rhs)
+    with pytest.raises(blfmm.InvalidArgument):
+        S.solve_interpolation(S.InterpolationProblem(k, None, rhs))
+    with pytest.raises(blfmm.InvalidArgument):
+        S.solve_interpolation(S.InterpolationProblem(k, ps, rhs[:-1]))
+    with pytest.raises(blfmm.InvalidArgument):
+        S.solve_interpolation(S.InterpolationProblem(k, ps, rhs, tol=0.0))
