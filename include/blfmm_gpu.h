@@ -171,6 +171,21 @@ int blfmm_get_stage_times(const blfmm_plan* plan, blfmm_stage_times* t);
 int blfmm_partition(const double* cost, long long n, int world, long long* bounds);
 int blfmm_plan_owned_points(const blfmm_plan* plan, long long* idx);
 
+/* Exchange mode (world > 1, leaf level >= 3): the upsweep is partitioned too.
+ * Each rank runs P2M on its leaves plus a two-leaf halo (complete multipoles
+ * at levels L and L-1 where its downsweep reads them) and writes PARTIAL
+ * multipoles of levels 1..L-2 (own leaves only, disjoint across ranks) into a
+ * caller-bound device buffer of blfmm_plan_exchange_size doubles. The caller
+ * all-reduces (sum) that buffer across ranks — the upper-level expansion
+ * exchange over NCCL / NVLink — between the two halves:
+ *   blfmm_execute_upsweep -> all-reduce(buffer) -> blfmm_execute_downsweep
+ * and then all-reduces the outputs as above. */
+int blfmm_plan_exchange_size(const blfmm_plan* plan, long long* n_doubles);
+int blfmm_plan_bind_exchange(blfmm_plan* plan, double* d_buffer);
+int blfmm_execute_upsweep(blfmm_plan* plan, const double* d_lambda, void* stream);
+int blfmm_execute_downsweep(blfmm_plan* plan, double* d_out, blfmm_stats* stats,
+                            void* stream);
+
 /* Independent O(N^2) check (direct_matvec, fmm.cpp:30-75): values for
  * n_targets target indices (NULL = all n) into HOST out. */
 int blfmm_direct(int d, long long n, const double* coords, int kernel_type,

@@ -83,6 +83,11 @@ EXPORTS = {
     "blfmm_partition": (ct.c_int, [ct.POINTER(ct.c_double), ct.c_longlong, ct.c_int,
                                    ct.POINTER(ct.c_longlong)]),
     "blfmm_plan_owned_points": (ct.c_int, [ct.c_void_p, ct.POINTER(ct.c_longlong)]),
+    "blfmm_plan_exchange_size": (ct.c_int, [ct.c_void_p, ct.POINTER(ct.c_longlong)]),
+    "blfmm_plan_bind_exchange": (ct.c_int, [ct.c_void_p, ct.c_void_p]),
+    "blfmm_execute_upsweep": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
+    "blfmm_execute_downsweep": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.POINTER(Stats),
+                                           ct.c_void_p]),
     "blfmm_direct": (ct.c_int, [ct.c_int, ct.c_longlong, ct.POINTER(ct.c_double), ct.c_int,
                                 ct.c_double, ct.POINTER(ct.c_double), ct.c_longlong,
                                 ct.POINTER(ct.c_longlong), ct.POINTER(ct.c_double), ct.c_int]),

@@ -367,6 +367,27 @@ class Plan:
             return SumStats(st.near_pairs, st.far_work, st.max_imag_residual)
         return None
 
+    # ---- multi-GPU exchange mode (blfmm_execute_upsweep / _downsweep)
+    def exchange_size(self) -> int:
+        """Doubles in the exchange buffer (0: no exchange mode)."""
+        v = ct.c_longlong()
+        _capi.check(_capi.lib().blfmm_plan_exchange_size(self._h, ct.byref(v)))
+        return v.value
+
+    def bind_exchange(self, d_buffer: int):
+        _capi.check(_capi.lib().blfmm_plan_bind_exchange(self._h, ct.c_void_p(d_buffer)))
+
+    def upsweep(self, d_lambda: int, stream=None):
+        _capi.check(_capi.lib().blfmm_execute_upsweep(self._h, ct.c_void_p(d_lambda), stream))
+
+    def downsweep(self, d_out: int, stream=None, stats: bool = False):
+        st = _capi.Stats() if stats else None
+        _capi.check(_capi.lib().blfmm_execute_downsweep(
+            self._h, ct.c_void_p(d_out), ct.byref(st) if st is not None else None, stream))
+        if st is not None:
+            return SumStats(st.near_pairs, st.far_work, st.max_imag_residual)
+        return None
+
     def set_profiling(self, on: bool = True):
         _capi.check(_capi.lib().blfmm_set_profiling(self._h, int(on)))
 

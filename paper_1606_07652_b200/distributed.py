@@ -8,9 +8,13 @@ near field for its own range only, writing zeros elsewhere. The exchange is
 one all-reduce(sum) of the output vector over NCCL (NVLink) — the ranks'
 supports are disjoint, so the sum is the matvec bit for bit.
 
-Round-1 scope: the upsweep (P2M + M2M) is replicated on every rank instead
-of exchanging leaf / coarse-level multipoles (the halo + coarse all-reduce
-design is the next step).
+Exchange mode (leaf level >= 3, the default here): the upsweep is partitioned
+as well. Each rank runs P2M on its leaves plus a two-leaf halo, keeps complete
+multipoles at levels L and L-1 where its downsweep reads them, and writes
+partial multipoles of levels 1..L-2 (its own leaves only) into an exchange
+buffer; one NCCL all-reduce of that buffer is the upper-level expansion
+exchange, after which the downsweep runs. Without exchange mode
+(blfmm_execute on a world > 1 plan) the upsweep is replicated instead.
 """
 from __future__ import annotations
 
@@ -52,13 +56,21 @@ class ShardedMatvec:
     """u = A lambda over `world` ranks (torch.distributed process group)."""
 
     def __init__(self, ps: PointSet, leaf_level: int, kernel: RadialKernel, sigma: float,
-                 m_per_dim: int, nrhs: int = 1, group=None, device: int = -1):
+                 m_per_dim: int, nrhs: int = 1, group=None, device: int = -1,
+                 exchange: bool = True, rank: int | None = None, world: int | None = None):
+        import torch
         import torch.distributed as dist
         self.group = group
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        init = dist.is_available() and dist.is_initialized()
+        self.rank = rank if rank is not None else (dist.get_rank(group) if init else 0)
+        self.world = world if world is not None else (dist.get_world_size(group) if init else 1)
         self.plan = Plan(ps, leaf_level, kernel, sigma, m_per_dim, nrhs=nrhs, device=device,
                          rank=self.rank, world=self.world)
+        self.xbuf = None
+        if exchange and self.world > 1 and self.plan.exchange_size() > 0:
+            dev = torch.device("cuda", device) if device >= 0 else torch.device("cuda")
+            self.xbuf = torch.zeros(self.plan.exchange_size(), dtype=torch.float64, device=dev)
+            self.plan.bind_exchange(self.xbuf.data_ptr())
 
     def owned_points(self) -> np.ndarray:
         inf = self.plan.info()
@@ -69,8 +81,15 @@ class ShardedMatvec:
         return idx
 
     def device(self, lam, out, stream=None):
-        """lam / out: device tensors [nrhs, n]; out is assembled on every rank."""
-        self.plan.execute_device(lam.data_ptr(), out.data_ptr(), stream=stream)
+        """lam / out: device tensors [nrhs, n]; out is assembled on every rank.
+        Stream ordering: the library orders its work after / before `stream`
+        (NULL = the default stream), where the NCCL calls are enqueued."""
+        if self.xbuf is not None:
+            self.plan.upsweep(lam.data_ptr(), stream=stream)
+            assemble(self.xbuf, self.group)  # upper-level expansion exchange
+            self.plan.downsweep(out.data_ptr(), stream=stream)
+        else:
+            self.plan.execute_device(lam.data_ptr(), out.data_ptr(), stream=stream)
         if self.world > 1:
             assemble(out, self.group)
         return out

@@ -328,3 +328,43 @@ def test_batched_rhs_near_field_path(blfmm, oracle, nr):
     p1 = blfmm.Plan(ps, 3, k, W.sigma, 8, nrhs=1)
     for r in (0, 7, nr - 1):
         assert rel_l2(vb[r], p1.execute(w[r]).values) <= 1e-14
+
+
+@pytest.mark.parametrize("name,n,leaf", [("P3", 80000, 4), ("P2p", 40000, 4), ("P4", 60000, 5)])
+def test_exchange_mode_assembles_to_full(blfmm, name, n, leaf):
+    """Partitioned upsweep: per-rank halo P2M + partial coarse multipoles; the
+    all-reduce of the exchange buffers (emulated here by a device sum over the
+    ranks, all on one GPU, no collective) followed by the downsweeps and the
+    output sum reproduces the single-plan matvec."""
+    import ctypes as ct
+    import torch
+    W = I.WORKLOADS[name]
+    x, w = W.make(n)
+    k = blfmm.parse_kernel_spec(W.kernel)
+    ps = blfmm.PointSet(W.d, x)
+    full = blfmm.Plan(ps, leaf, k, W.sigma, W.m).execute(w).values
+    lam = torch.from_numpy(np.ascontiguousarray(w.reshape(1, -1))).cuda()
+    for world in (2, 3, 5):
+        plans, bufs = [], []
+        for rank in range(world):
+            pl = blfmm.Plan(ps, leaf, k, W.sigma, W.m, rank=rank, world=world)
+            nx = pl.exchange_size()
+            assert nx > 0
+            b = torch.zeros(nx, dtype=torch.float64, device="cuda")
+            pl.bind_exchange(b.data_ptr())
+            plans.append(pl)
+            bufs.append(b)
+        for pl in plans:
+            pl.upsweep(lam.data_ptr())
+        torch.cuda.synchronize()
+        total = torch.stack(bufs).sum(0)
+        for b in bufs:
+            b.copy_(total)
+        acc = torch.zeros_like(lam)
+        for pl in plans:
+            out = torch.empty_like(lam)
+            pl.downsweep(out.data_ptr())
+            torch.cuda.synchronize()
+            acc += out
+        got = acc.cpu().numpy()[0]
+        assert rel_l2(got, full) <= 1e-13, (world, rel_l2(got, full))
