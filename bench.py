@@ -150,11 +150,20 @@ def run_ours(args, W, world, rank, local):
 
     import paper_1606_07652_b200 as B
 
+    # test-only overrides: run the N>1 code path on a single-GPU box
+    # (BLFMM_BENCH_DEVICE pins every rank to one device; BLFMM_DIST_BACKEND=gloo
+    # keeps ranks that share a GPU from waiting on each other's kernels)
+    if os.environ.get("BLFMM_BENCH_DEVICE") is not None:
+        local = int(os.environ["BLFMM_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BLFMM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     x, w = W.make()
     n, nrhs = W.n, W.nrhs
     k = B.parse_kernel_spec(W.kernel)
@@ -367,12 +376,14 @@ def cpu_baseline(W, stride):
 def run_reference(args, W):
     from oracle import pyoracle as po
     cores = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    os.environ["OMP_NUM_THREADS"] = str(cores)  # torchrun exports 1
+    cores = po.set_threads(cores)
     kind = "port"
     if W.d <= 2 and po.ref_available():
         kind = "reference"
     times = []
-    stride = args.cpu_stride
+    # bounded sample: about 4 steps' worth of stride-32 sampling in total
+    stride = args.cpu_stride * max(1, math.ceil((args.steps + args.warmup) / 4))
     for s in range(args.warmup + args.steps):
         if kind == "reference" and W.nrhs == 1:
             x, w = W.make()
@@ -420,7 +431,9 @@ def main():
     line, clocks = run_ours(args, W, world, rank, local)
     line["clocks"] = clocks
     if rank == 0:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
+            from oracle import pyoracle as po
+            po.set_threads(os.cpu_count() or 1)
             t, secs = cpu_baseline(W, args.cpu_stride)
             line["cpu_baseline"] = {
                 "value": W.nrhs * float(W.n) ** 2 / t, "unit": UNIT,

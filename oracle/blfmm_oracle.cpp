@@ -940,6 +940,13 @@ extern "C" {
 
 const char* orc_last_error() { return g_err.c_str(); }
 
+// bench.py's CPU legs: use every host thread even when a launcher (torchrun)
+// exported OMP_NUM_THREADS=1 before this library was loaded.
+void orc_set_num_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+}
+int orc_get_max_threads() { return omp_get_max_threads(); }
+
 std::uint64_t orc_hash64(std::uint64_t x) {  // common.hpp:45-50
   x += 0x9e3779b97f4a7c15ull;
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;

@@ -207,6 +207,12 @@ def tree_lists(x, leaf, level, which, lo=None, hi=None):
     return np.split(ids, np.cumsum(counts)[:-1])
 
 
+def set_threads(n: int) -> int:
+    """omp_set_num_threads for the oracle (returns the resulting max threads)."""
+    lib().orc_set_num_threads(int(n))
+    return lib().orc_get_max_threads()
+
+
 def sum_il(d, leaf, level):
     return lib().orc_sum_il(d, leaf, level)
 
