@@ -1,2 +1,1 @@
-for h in 0 1; do echo "HERM=$h"; BLFMM_HERMITIAN=$h python tools/run_steps.py --steps 3 2>&1 | tail -1; done
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
+for b in 2 3 4 5; do BLFMM_COUPLE_MINB=$b python tools/run_steps.py --steps 3 2>&1 | tail -1 | sed "s/^/minb$b /"; done
