@@ -280,7 +280,7 @@ def run_ours(args, W, world, rank, local):
     evals = nrhs * float(n) * float(n)
     value = evals / (ms / 1e3)
     pk = peaks()
-    m2m_b, m2l_b = far_bytes(info, K, nrhs)
+    m2m_b, m2l_b = far_bytes(info, info.stored_nodes, nrhs)
     stage = {k_: {"ms": round(v[0], 4), "launches": v[1]} for k_, v in acc.items()}
     top = max(acc.items(), key=lambda kv: kv[1][0])[0]
     hbm_peak = pk.get("hbm_gbs", 6650.0)
@@ -288,7 +288,7 @@ def run_ours(args, W, world, rank, local):
     m2l_ms = acc.get("m2l_l2l", [0, 0])[0]
     if m2l_ms > 0:
         ach = m2l_b / (m2l_ms / 1e3) / 1e9
-        roof = {"kernel": "k_couple (M2L + fused L2L)", "bound": "hbm", "achieved": round(ach, 1),
+        roof = {"kernel": "k_couple* (M2L + fused L2L)", "bound": "hbm", "achieved": round(ach, 1),
                 "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
                 "traffic": load_traffic("k_couple"),
                 "algorithmic_bytes": m2l_b,
@@ -348,14 +348,18 @@ def ct_stream(stream):
     return ct.c_void_p(stream.cuda_stream)
 
 
-def load_traffic(kernel):
-    """DRAM bytes (read + write) of `kernel` per matvec (all its launches of
-    one step, matching `achieved`), from the committed ncu capture
-    profiles/r01_ncu_step_dram.json, or None."""
+TRAFFIC_PROFILE = os.path.join(ROOT, "profiles", "r01_ncu_step_dram.json")
+
+
+def load_traffic(prefix):
+    """DRAM bytes (read + write) per matvec of the kernels whose name starts
+    with `prefix` (all launches of one step, matching `achieved`), from the
+    committed ncu capture (tools/ncu_dram_summary.py), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_step_dram.json")) as f:
+        with open(TRAFFIC_PROFILE) as f:
             s = json.load(f)
-        return s["kernels"][kernel]["dram_bytes_total"]
+        hits = [v["dram_bytes_total"] for k_, v in s["kernels"].items() if k_.startswith(prefix)]
+        return float(sum(hits)) if hits else None
     except Exception:
         return None
 

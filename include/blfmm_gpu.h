@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define BLFMM_GPU_ABI_VERSION 1
+#define BLFMM_GPU_ABI_VERSION 2
 
 /* Status codes (reference exception class in parentheses). */
 enum blfmm_status {
@@ -103,6 +103,8 @@ typedef struct blfmm_plan_info {
   long long owned_begin, owned_end; /* owned sorted-point range (multi-GPU) */
   double plan_seconds;
   long long device_bytes;
+  long long stored_nodes;   /* complex coefficients stored per expansion: K, or
+                               the Hermitian half spectrum (3-D, M = 16: 2528) */
 } blfmm_plan_info;
 
 /* Per-stage device times of the last execute (CUDA events on the launch
