@@ -1,1 +1,1 @@
-for v in 1 5; do BLFMM_COUPLE_VARIANT=$v python tools/run_steps.py --steps 3 2>&1 | tail -1 | sed "s/^/v$v /"; done
+for f in 0 1; do BLFMM_FUSE_NEAR_M2M=$f python tools/time_step.py --tag fuse$f 2>&1 | tail -1; done
