@@ -58,7 +58,9 @@ enum blfmm_kernel_type {
   BLFMM_KERNEL_WENDLAND31 = 5
 };
 
-/* GridMode (mlfmm.hpp:21-28). Only `shared` is executable (EDOMAIN else). */
+/* GridMode (mlfmm.hpp:21-28). `scaled` (per-level halved band, Lagrange
+ * M2M/L2L transfers, direct interaction-list couple) needs world == 1 and
+ * M^d <= 6400 (EDOMAIN else). */
 enum blfmm_grid_mode { BLFMM_GRID_SHARED = 0, BLFMM_GRID_SCALED = 1 };
 
 typedef struct blfmm_plan blfmm_plan;
@@ -75,11 +77,12 @@ typedef struct blfmm_plan_desc {
   int m_per_dim;          /* quadrature nodes per axis M (>= 2); K = M^d */
   int leaf_level;         /* uniform tree depth L (>= 2, d*L <= 24) */
   int grid_mode;          /* enum blfmm_grid_mode */
-  int stencil_k;          /* scaled-mode stencil (ignored for shared) */
+  int stencil_k;          /* scaled-mode Lagrange stencil, clamped to M (ignored for shared) */
   int nrhs;               /* right-hand sides per execute (>= 1) */
   int device;             /* CUDA device ordinal, -1 = current */
   const double* c_table;  /* optional HOST override of C(xi_m), K doubles
-                             (LowRankFactors::c_vals); NULL = compute */
+                             (LowRankFactors::c_vals); scaled mode: (L-1)*K
+                             doubles, levels 2..L in order; NULL = compute */
   int rank;               /* multi-GPU: this plan's Morton-range index ... */
   int world;              /* ... of `world` ranges (1 = whole problem) */
 } blfmm_plan_desc;

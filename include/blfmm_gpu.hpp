@@ -53,7 +53,7 @@ struct PlanHandle {
   blfmm_plan* p = nullptr;
   const PointSet* ps = nullptr;
   std::size_t n = 0;
-  int leaf = 0, m = 0, mode = 0;
+  int leaf = 0, m = 0, mode = 0, stencil = 10;
   double sigma = 0.0;
   RadialKernel kernel;
   std::vector<double> c_vals;
@@ -63,11 +63,13 @@ struct PlanHandle {
 };
 
 inline blfmm_plan* plan_for(const PointSet& ps, const BoxTree& tree, const RadialKernel& k,
-                            double sigma, int m, const std::vector<double>& c_vals) {
+                            double sigma, int m, const std::vector<double>& c_vals,
+                            int mode = BLFMM_GRID_SHARED, int stencil_k = 10) {
   thread_local std::unique_ptr<PlanHandle> cache;
   if (cache && cache->ps == &ps && cache->n == ps.pts.size() && cache->leaf == tree.leaf_level &&
       cache->m == m && cache->sigma == sigma && cache->kernel.type == k.type &&
-      cache->kernel.shape == k.shape && cache->c_vals == c_vals)
+      cache->kernel.shape == k.shape && cache->c_vals == c_vals && cache->mode == mode &&
+      cache->stencil == stencil_k)
     return cache->p;
   cache.reset(new PlanHandle());
   const int d = ps.d;
@@ -88,8 +90,8 @@ inline blfmm_plan* plan_for(const PointSet& ps, const BoxTree& tree, const Radia
   desc.sigma = sigma;
   desc.m_per_dim = m;
   desc.leaf_level = tree.leaf_level;
-  desc.grid_mode = BLFMM_GRID_SHARED;
-  desc.stencil_k = 10;
+  desc.grid_mode = mode;
+  desc.stencil_k = stencil_k;
   desc.nrhs = 1;
   desc.device = -1;
   desc.c_table = c_vals.data();  // the reference's own C(xi_m): bit-identical spectrum
@@ -102,6 +104,8 @@ inline blfmm_plan* plan_for(const PointSet& ps, const BoxTree& tree, const Radia
   cache->sigma = sigma;
   cache->kernel = k;
   cache->c_vals = c_vals;
+  cache->mode = mode;
+  cache->stencil = stencil_k;
   return cache->p;
 }
 
@@ -126,9 +130,16 @@ inline SumResult mlfmm_matvec(const SumRequest& req, const BoxTree& tree,
     throw std::invalid_argument("weight count != point count");
   if (grids.d != ps.d || grids.leaf_level != tree.leaf_level)
     throw std::invalid_argument("grids incompatible with tree/points");
-  if (grids.mode != GridMode::shared)
-    throw std::domain_error("GridMode::scaled is not implemented on the GPU path");
   const auto& g = grids.grids[tree.leaf_level];
+  if (grids.mode == GridMode::scaled) {
+    // the reference's own per-level C tables, levels 2..L in order
+    std::vector<double> c;
+    for (int l = 2; l <= tree.leaf_level; ++l)
+      c.insert(c.end(), grids.factors[l].c_vals.begin(), grids.factors[l].c_vals.end());
+    blfmm_plan* p = plan_for(ps, tree, grids.kernel, g.sigma, g.m_per_dim, c, BLFMM_GRID_SCALED,
+                             grids.stencil_k);
+    return run(p, req.weights, false);
+  }
   blfmm_plan* p = plan_for(ps, tree, grids.kernel, g.sigma, g.m_per_dim,
                            grids.factors[tree.leaf_level].c_vals);
   return run(p, req.weights, false);

@@ -24,7 +24,7 @@ static double rel_l2(const std::vector<double>& a, const std::vector<double>& b)
 }
 
 static int run_case(const char* name, const std::string& spec, int d, int n, double sigma, int m,
-                    int leaf, bool single) {
+                    int leaf, bool single, GridMode mode = GridMode::shared, int stencil = 10) {
   PointSet ps;
   ps.d = d;
   for (int i = 0; i < n; ++i)
@@ -40,7 +40,7 @@ static int run_case(const char* name, const std::string& spec, int d, int n, dou
     ref = fmm_matvec_single(req, tree);
     gpu = blfmm::gpu::fmm_matvec_single(req, tree);
   } else {
-    LevelGrids grids = make_level_grids(k, sigma, m, d, leaf, GridMode::shared, 10);
+    LevelGrids grids = make_level_grids(k, sigma, m, d, leaf, mode, stencil);
     ref = mlfmm_matvec(req, tree, grids);
     gpu = blfmm::gpu::mlfmm_matvec(req, tree, grids);
     // second call reuses the cached plan (solver pattern)
@@ -66,6 +66,10 @@ int main() {
   fails += run_case("imq:c=0.1 2D N=8192", "imq:c=0.1", 2, 8192, M_PI, 16, 4, false);
   fails += run_case("imq:c=1 1D N=1024 L=5", "imq:c=1", 1, 1024, M_PI, 64, 5, false);
   fails += run_case("single-level imq:c=1 2D", "imq:c=1", 2, 2048, M_PI, 12, 3, true);
+  fails += run_case("scaled grids imq:c=1 2D stencil 10", "imq:c=1", 2, 4096, M_PI, 16, 4,
+                    false, GridMode::scaled, 10);
+  fails += run_case("scaled grids gaussian:c=1 1D stencil 6", "gaussian:c=1", 1, 2048, M_PI, 16,
+                    6, false, GridMode::scaled, 6);
   // error mapping: mismatched grids -> std::invalid_argument
   try {
     PointSet ps;

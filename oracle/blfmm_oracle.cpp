@@ -46,6 +46,7 @@ struct Kernel {
 };
 
 thread_local std::string g_err;
+int g_mode = 0, g_stencil = 10;
 
 // ---------------------------------------------------------------- kernels
 // eval_kernel, kernels.cpp:131-161
@@ -563,6 +564,120 @@ Grid make_grid(double sigma, int M, int d) {
   return g;
 }
 
+// Per-axis k-point Lagrange interpolation (lagrange_matrix, mlfmm.cpp:42-80):
+// row r holds the weights of source nodes lo[r] .. lo[r]+k-1 at target r.
+struct Interp {
+  int rows = 0, cols = 0, k = 0;
+  std::vector<int> lo;
+  std::vector<double> w;  // rows*k
+};
+Interp lagrange(const std::vector<double>& src, const std::vector<double>& tgt, int k) {
+  int n = static_cast<int>(src.size());
+  if (k < 1 || k > n) throw std::invalid_argument("stencil size out of range");
+  for (int i = 1; i < n; ++i)
+    if (!(src[i] > src[i - 1])) throw std::invalid_argument("source nodes must be strictly increasing");
+  Interp P;
+  P.rows = static_cast<int>(tgt.size());
+  P.cols = n;
+  P.k = k;
+  P.lo.resize(P.rows);
+  P.w.resize((size_t)P.rows * k);
+  for (int r = 0; r < P.rows; ++r) {
+    double t = tgt[r];
+    int lo = static_cast<int>(std::lower_bound(src.begin(), src.end(), t) - src.begin()) - k / 2;
+    lo = std::clamp(lo, 0, n - k);
+    while (lo > 0 && t - src[lo - 1] < src[lo + k - 1] - t) --lo;
+    while (lo + k < n && src[lo + k] - t < t - src[lo]) ++lo;
+    P.lo[r] = lo;
+    for (int j = 0; j < k; ++j) {
+      double w = 1.0;
+      for (int l = 0; l < k; ++l) {
+        if (l == j) continue;
+        w *= (t - src[lo + l]) / (src[lo + j] - src[lo + l]);
+      }
+      P.w[(size_t)r * k + j] = w;
+    }
+  }
+  return P;
+}
+std::vector<double> axis_nodes(double sigma, int M) {  // mlfmm.cpp:15-20
+  std::vector<double> v(M);
+  double dxi = 2.0 * sigma / M;
+  for (int m = 0; m < M; ++m) v[m] = -sigma + m * dxi;
+  return v;
+}
+
+// make_level_grids (mlfmm.cpp:112-142): shared mode reuses the leaf grid and
+// C table at every level; scaled mode halves the band per coarsening step
+// (sigma_{l-1} = sigma_l / 2, weights / 2^d), one C table per level and the
+// child -> parent Lagrange transfer P[l] (grid l nodes -> grid l-1 nodes).
+struct Grids {
+  bool scaled = false;
+  int k = 0;
+  std::vector<Grid> g;                 // [0..L]
+  std::vector<std::vector<double>> c;  // [0..L]
+  std::vector<Interp> P;               // [3..L]
+  std::vector<double> sig;             // band per level
+};
+Grids make_grids(const Kernel& kern, double sigma, int M, int d, int L, int mode, int stencil,
+                 const double* c_in) {
+  Grids G;
+  G.scaled = mode == 1;
+  G.k = std::min(stencil, M);
+  G.g.resize(L + 1);
+  G.c.resize(L + 1);
+  G.sig.assign(L + 1, sigma);
+  long K = 1;
+  for (int i = 0; i < d; ++i) K *= M;
+  double s = sigma;
+  for (int l = L; l >= 2; --l) {
+    G.sig[l] = s;
+    G.g[l] = make_grid(s, M, d);
+    if (!G.scaled && l < L) {
+      G.c[l] = G.c[L];
+    } else if (c_in) {  // caller tables: one per level (levels 2..L) in scaled mode
+      const double* src = G.scaled ? c_in + (long)(l - 2) * K : c_in;
+      G.c[l].assign(src, src + K);
+    } else {
+      G.c[l] = c_table(kern, s, M, d);
+    }
+    if (G.scaled) s = s / 2.0;
+  }
+  if (G.scaled) {
+    G.P.resize(L + 1);
+    for (int l = 3; l <= L; ++l)
+      G.P[l] = lagrange(axis_nodes(G.sig[l], M), axis_nodes(G.sig[l - 1], M), G.k);
+  }
+  return G;
+}
+
+// Tensor application of P along every axis (interp_apply, mlfmm.cpp:146-171;
+// axis 0 first) and of P^T (interp_apply_transpose, 173-197).
+void interp_tensor(const Interp& P, int d, int M, const std::vector<C>& x, std::vector<C>& out,
+                   bool transpose) {
+  std::vector<C> cur = x, nxt(x.size());
+  long K = (long)cur.size();
+  for (int ax = 0; ax < d; ++ax) {
+    long stride = 1;
+    for (int q = ax + 1; q < d; ++q) stride *= M;
+    std::fill(nxt.begin(), nxt.end(), C(0.0, 0.0));
+    for (long base = 0; base < K; ++base) {
+      if ((base / stride) % M != 0) continue;  // base has axis index 0
+      for (int r = 0; r < P.rows; ++r)
+        for (int j = 0; j < P.k; ++j) {
+          const int c = P.lo[r] + j;
+          const double w = P.w[(size_t)r * P.k + j];
+          if (!transpose)
+            nxt[base + r * stride] += w * cur[base + c * stride];
+          else
+            nxt[base + c * stride] += w * cur[base + r * stride];
+        }
+    }
+    std::swap(cur, nxt);
+  }
+  out = std::move(cur);
+}
+
 using Level = std::vector<std::vector<C>>;  // [box] -> K coeffs (empty = 0)
 
 struct Stats {
@@ -595,9 +710,10 @@ std::vector<long> occupied(const Tree& t, int l, int stride) {
 }
 
 // upsweep, mlfmm.cpp:201-266 (shared grids)
-std::vector<Level> upsweep(const Problem& p, const Tree& t, const Grid& g,
+std::vector<Level> upsweep(const Problem& p, const Tree& t, const Grids& G,
                            const double* w, Sampler* s) {
   int L = t.L, stride = s ? s->stride : 1;
+  const Grid& g = G.g[L];
   std::vector<Level> ex(L + 1);
   for (int l = 2; l <= L; ++l) ex[l].resize(t.count(l));
   if (stride > 1)  // sampled timing: every occupied box holds (zero) data so
@@ -633,6 +749,8 @@ std::vector<Level> upsweep(const Problem& p, const Tree& t, const Grid& g,
         t.center(l - 1, pb, xp);
         auto& out = ex[l - 1][pb];
         out.assign(g.K, C(0.0, 0.0));
+        const Grid& gp = G.g[l - 1];
+        std::vector<C> tmp;
         for (long c : t.children(l - 1, pb)) {
           const auto& vc = ex[l][c];
           if (vc.empty()) continue;
@@ -640,8 +758,14 @@ std::vector<Level> upsweep(const Problem& p, const Tree& t, const Grid& g,
           t.center(l, c, xc);
           double r[3] = {0, 0, 0};
           for (int k = 0; k < p.d; ++k) r[k] = xp[k] - xc[k];
-          for (long m = 0; m < g.K; ++m)
-            out[m] += std::polar(1.0, dot(p.d, &g.nodes[m * 3], r)) * vc[m];
+          if (!G.scaled) {
+            for (long m = 0; m < g.K; ++m)
+              out[m] += std::polar(1.0, dot(p.d, &gp.nodes[m * 3], r)) * vc[m];
+          } else {  // mlfmm.cpp:256-261: interpolate to the parent grid, then shift
+            interp_tensor(G.P[l], p.d, p.M, vc, tmp, false);
+            for (long m = 0; m < g.K; ++m)
+              out[m] += std::polar(1.0, dot(p.d, &gp.nodes[m * 3], r)) * tmp[m];
+          }
         }
       }
     }
@@ -651,10 +775,10 @@ std::vector<Level> upsweep(const Problem& p, const Tree& t, const Grid& g,
 }
 
 // couple, mlfmm.cpp:268-299
-std::vector<Level> couple(const Problem& p, const Tree& t, const Grid& g,
-                          const std::vector<double>& cv,
+std::vector<Level> couple(const Problem& p, const Tree& t, const Grids& G,
                           const std::vector<Level>& mult, Sampler* s) {
   int L = t.L, stride = s ? s->stride : 1;
+  const Grid& g = G.g[L];
   std::vector<Level> loc(L + 1);
   if (stride > 1)
     for (int l = 2; l <= L; ++l) {
@@ -672,6 +796,8 @@ std::vector<Level> couple(const Problem& p, const Tree& t, const Grid& g,
         t.center(l, a, xa);
         auto& out = loc[l][a];
         if (out.empty()) out.assign(g.K, C(0.0, 0.0));
+        const Grid& gl = G.g[l];
+        const std::vector<double>& cv = G.c[l];
         for (long b : t.interaction(l, a)) {
           const auto& vb = mult[l][b];
           if (vb.empty()) continue;
@@ -680,7 +806,7 @@ std::vector<Level> couple(const Problem& p, const Tree& t, const Grid& g,
           double r[3] = {0, 0, 0};
           for (int k = 0; k < p.d; ++k) r[k] = xa[k] - xb[k];
           for (long m = 0; m < g.K; ++m)
-            out[m] += cv[m] * std::polar(1.0, dot(p.d, &g.nodes[m * 3], r)) * vb[m];
+            out[m] += cv[m] * std::polar(1.0, dot(p.d, &gl.nodes[m * 3], r)) * vb[m];
         }
       }
     }
@@ -690,10 +816,11 @@ std::vector<Level> couple(const Problem& p, const Tree& t, const Grid& g,
 }
 
 // downsweep, mlfmm.cpp:301-359
-void downsweep(const Problem& p, const Tree& t, const Grid& g,
+void downsweep(const Problem& p, const Tree& t, const Grids& G,
                const std::vector<Level>& locals, double* out, double* max_imag,
                Sampler* s, std::vector<Level>* acc_out = nullptr) {
   int L = t.L, stride = s ? s->stride : 1;
+  const Grid& g = G.g[L];
   std::vector<Level> acc;
   double tcopy = timed([&] { acc = locals; });  // mlfmm.cpp:305
   double tl = timed([&] {
@@ -706,6 +833,10 @@ void downsweep(const Problem& p, const Tree& t, const Grid& g,
         if (lp.empty()) continue;
         double xp[3];
         t.center(l, pb, xp);
+        const Grid& gc = G.g[l + 1];
+        const double wratio = G.g[l].weight / gc.weight;  // uniform weights
+        std::vector<C> tmp;
+        if (G.scaled) interp_tensor(G.P[l + 1], p.d, p.M, lp, tmp, true);
         for (long c : t.children(l, pb)) {
           auto& lc = acc[l + 1][c];
           if (lc.empty()) continue;  // unoccupied child: never reaches a point
@@ -713,8 +844,13 @@ void downsweep(const Problem& p, const Tree& t, const Grid& g,
           t.center(l + 1, c, xc);
           double r[3] = {0, 0, 0};
           for (int k = 0; k < p.d; ++k) r[k] = xc[k] - xp[k];
-          for (long m = 0; m < g.K; ++m)
-            lc[m] += std::polar(1.0, dot(p.d, &g.nodes[m * 3], r)) * lp[m];
+          if (!G.scaled) {
+            for (long m = 0; m < g.K; ++m)
+              lc[m] += std::polar(1.0, dot(p.d, &gc.nodes[m * 3], r)) * lp[m];
+          } else {  // mlfmm.cpp:331-337: anterpolate, weight ratio, shift
+            for (long m = 0; m < g.K; ++m)
+              lc[m] += wratio * std::polar(1.0, dot(p.d, &gc.nodes[m * 3], r)) * tmp[m];
+          }
         }
       }
     }
@@ -768,17 +904,17 @@ long long sum_il_sizes(const Tree& t, int l) {
 }
 
 // mlfmm_matvec, mlfmm.cpp:361-406
-void mlfmm(const Problem& p, const std::vector<double>& cv, const double* w,
-           double* out, Stats* st, Sampler* s) {
+void mlfmm(const Problem& p, const Grids& G, const double* w, double* out, Stats* st,
+           Sampler* s) {
   if (p.L < 2) throw std::invalid_argument("leaf_level must be >= 2");
   Tree t = build_tree(p, p.L);
-  Grid g = make_grid(p.sigma, p.M, p.d);
+  const Grid& g = G.g[p.L];
   std::fill(out, out + p.n, 0.0);
-  auto mult = upsweep(p, t, g, w, s);
-  auto loc = couple(p, t, g, cv, mult, s);
+  auto mult = upsweep(p, t, G, w, s);
+  auto loc = couple(p, t, G, mult, s);
   mult.clear();
   double imag = 0.0;
-  downsweep(p, t, g, loc, out, &imag, s);
+  downsweep(p, t, G, loc, out, &imag, s);
   loc.clear();
   int L = t.L, stride = s ? s->stride : 1;
   long long near = 0;
@@ -940,6 +1076,14 @@ extern "C" {
 
 const char* orc_last_error() { return g_err.c_str(); }
 
+// GridMode for the following orc_mlfmm / orc_expansions calls (0 shared,
+// 1 scaled) and the Lagrange stencil size (make_level_grids' stencil_k).
+// In scaled mode a caller C table holds one K-entry table per level 2..L.
+void orc_set_grid_mode(int mode, int stencil_k) {
+  g_mode = mode;
+  g_stencil = stencil_k;
+}
+
 // bench.py's CPU legs: use every host thread even when a launcher (torchrun)
 // exported OMP_NUM_THREADS=1 before this library was loaded.
 void orc_set_num_threads(int n) {
@@ -1000,16 +1144,13 @@ int orc_mlfmm(int d, long n, const double* x, const double* lo,
               int stride, double* stage_seconds) {
   return guard([&] {
     Problem p = make_problem(d, n, x, lo, hi, ktype, shape, sigma, M, L);
-    long K = 1;
-    for (int i = 0; i < d; ++i) K *= M;
-    std::vector<double> cv = c_in ? std::vector<double>(c_in, c_in + K)
-                                  : c_table(p.k, sigma, M, d);
+    Grids G = make_grids(p.k, sigma, M, d, L, g_mode, g_stencil, c_in);
     Sampler smp;
     smp.stride = stride > 0 ? stride : 1;
     double im = 0.0;
     for (int r = 0; r < nrhs; ++r) {
       Stats st{};
-      mlfmm(p, cv, w + (long)r * n, out + (long)r * n, &st, &smp);
+      mlfmm(p, G, w + (long)r * n, out + (long)r * n, &st, &smp);
       if (near) *near = st.near_pairs;
       if (far) *far = st.far_work;
       im = std::max(im, st.max_imag);
@@ -1067,20 +1208,19 @@ int orc_expansions(int d, long n, const double* x, const double* lo,
   return guard([&] {
     Problem p = make_problem(d, n, x, lo, hi, ktype, shape, sigma, M, L);
     Tree t = build_tree(p, L);
-    Grid g = make_grid(sigma, M, d);
-    std::vector<double> cv = c_in ? std::vector<double>(c_in, c_in + g.K)
-                                  : c_table(p.k, sigma, M, d);
-    auto mult = upsweep(p, t, g, w, nullptr);
+    Grids G = make_grids(p.k, sigma, M, d, L, g_mode, g_stencil, c_in);
+    const Grid& g = G.g[L];
+    auto mult = upsweep(p, t, G, w, nullptr);
     std::vector<Level> src;
     if (kind == 0) {
       src = std::move(mult);
     } else {
-      auto loc = couple(p, t, g, cv, mult, nullptr);
+      auto loc = couple(p, t, G, mult, nullptr);
       if (kind == 1) {
         src = std::move(loc);
       } else {
         std::vector<double> dummy(n, 0.0);
-        downsweep(p, t, g, loc, dummy.data(), nullptr, nullptr, &src);
+        downsweep(p, t, G, loc, dummy.data(), nullptr, nullptr, &src);
       }
     }
     long cnt = t.count(level);

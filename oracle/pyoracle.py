@@ -125,8 +125,12 @@ def c_table(spec, sigma, m, d):
 
 
 def mlfmm(x, w, spec, sigma, m, leaf, lo=None, hi=None, c_table_in=None,
-          stride=1):
-    """Returns (values [nrhs,n] or [n], stats dict, stage_seconds[6])."""
+          stride=1, mode=0, stencil=10):
+    """Returns (values [nrhs,n] or [n], stats dict, stage_seconds[6]).
+    mode 1 = scaled grids (c_table_in then holds levels 2..leaf)."""
+    if mode != 0:
+        with grid_mode(mode, stencil):
+            return mlfmm(x, w, spec, sigma, m, leaf, lo, hi, c_table_in, stride)
     x = np.ascontiguousarray(x, dtype=np.float64)
     n, d = x.shape
     w = np.ascontiguousarray(w, dtype=np.float64)
@@ -176,7 +180,10 @@ def direct(x, w, spec, targets=None):
 
 
 def expansions(x, w, spec, sigma, m, leaf, level, kind, lo=None, hi=None,
-               c_table_in=None):
+               c_table_in=None, mode=0, stencil=10):
+    if mode != 0:
+        with grid_mode(mode, stencil):
+            return expansions(x, w, spec, sigma, m, leaf, level, kind, lo, hi, c_table_in)
     x = np.ascontiguousarray(x, dtype=np.float64)
     n, d = x.shape
     w = np.ascontiguousarray(w, dtype=np.float64)
@@ -207,6 +214,25 @@ def tree_lists(x, leaf, level, which, lo=None, hi=None):
     return np.split(ids, np.cumsum(counts)[:-1])
 
 
+class grid_mode:
+    """Context: GridMode (0 shared, 1 scaled) + stencil_k for the oracle and
+    the compiled reference (make_level_grids, mlfmm.hpp:61-63)."""
+
+    def __init__(self, mode=0, stencil=10):
+        self.mode, self.stencil = int(mode), int(stencil)
+
+    def __enter__(self):
+        lib().orc_set_grid_mode(self.mode, self.stencil)
+        if ref_available():
+            ref().ref_set_grid_mode(self.mode, self.stencil)
+        return self
+
+    def __exit__(self, *a):
+        lib().orc_set_grid_mode(0, 10)
+        if ref_available():
+            ref().ref_set_grid_mode(0, 10)
+
+
 def set_threads(n: int) -> int:
     """omp_set_num_threads for the oracle (returns the resulting max threads)."""
     lib().orc_set_num_threads(int(n))
@@ -234,7 +260,10 @@ def ref_eval_fourier(spec, xi, d):
     return out.value
 
 
-def ref_mlfmm(x, w, spec, sigma, m, leaf, lo=None, hi=None, reps=1):
+def ref_mlfmm(x, w, spec, sigma, m, leaf, lo=None, hi=None, reps=1, mode=0, stencil=10):
+    if mode != 0:
+        with grid_mode(mode, stencil):
+            return ref_mlfmm(x, w, spec, sigma, m, leaf, lo, hi, reps)
     x = np.ascontiguousarray(x, dtype=np.float64)
     n, d = x.shape
     assert d <= 2
@@ -275,7 +304,20 @@ def ref_direct(x, w, spec):
     return out, near.value
 
 
-def ref_expansions(x, w, spec, sigma, m, leaf, level, kind, lo=None, hi=None):
+def ref_level_c_tables(spec, sigma, m, d, leaf, mode=0, stencil=10):
+    """LevelGrids::factors[l].c_vals, l = 2..leaf, as [leaf-1, K]."""
+    out = np.zeros((leaf - 1, m ** d))
+    with grid_mode(mode, stencil):
+        _chk(ref().ref_level_c_tables(_spec_b(spec), ct.c_double(sigma), m, d, leaf,
+                                      _ptr(out)), "ref")
+    return out
+
+
+def ref_expansions(x, w, spec, sigma, m, leaf, level, kind, lo=None, hi=None, mode=0,
+                   stencil=10):
+    if mode != 0:
+        with grid_mode(mode, stencil):
+            return ref_expansions(x, w, spec, sigma, m, leaf, level, kind, lo, hi)
     x = np.ascontiguousarray(x, dtype=np.float64)
     n, d = x.shape
     w = np.ascontiguousarray(w, dtype=np.float64)

@@ -25,6 +25,8 @@ using namespace blfmm;
 namespace {
 
 thread_local std::string g_err;
+GridMode g_mode = GridMode::shared;  // ref_set_grid_mode
+int g_stencil = 10;
 
 template <class F>
 int guard(F&& f) {
@@ -71,6 +73,27 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
+// GridMode (0 shared, 1 scaled) and stencil_k of make_level_grids for the
+// following ref_mlfmm / ref_expansions / ref_level_c_tables calls.
+void ref_set_grid_mode(int mode, int stencil_k) {
+  g_mode = mode == 1 ? GridMode::scaled : GridMode::shared;
+  g_stencil = stencil_k;
+}
+
+// LevelGrids::factors[l].c_vals for l = 2..leaf, concatenated (K each).
+int ref_level_c_tables(const char* spec, double sigma, int m, int d, int leaf, double* out) {
+  return guard([&] {
+    LevelGrids grids = make_level_grids(parse_kernel_spec(spec), sigma, m, d, leaf, g_mode,
+                                        g_stencil);
+    size_t pos = 0;
+    for (int l = 2; l <= leaf; ++l) {
+      const auto& c = grids.factors[l].c_vals;
+      std::memcpy(out + pos, c.data(), c.size() * sizeof(double));
+      pos += c.size();
+    }
+  });
+}
+
 int ref_eval_fourier(const char* spec, double xi, int d, double* out) {
   return guard([&] { *out = eval_fourier(parse_kernel_spec(spec), xi, d).value; });
 }
@@ -99,9 +122,9 @@ int ref_direct(int d, int n, const double* x, const char* spec,
   });
 }
 
-// One multilevel matvec with tree + grids built inside (shared grids, the
-// mode both production callers force: blfmm_cli.cpp:384-385,
-// solver.cpp:286-287). When `seconds` is given it receives the wall time of
+// One multilevel matvec with tree + grids built inside (shared grids by
+// default, the mode both production callers force: blfmm_cli.cpp:384-385,
+// solver.cpp:286-287; ref_set_grid_mode selects scaled grids). When `seconds` is given it receives the wall time of
 // the mlfmm_matvec call alone (tree and grids prebuilt, the
 // bench_matvec.cpp:48-61 convention), best of `reps`.
 int ref_mlfmm(int d, int n, const double* x, const double* lo,
@@ -113,7 +136,7 @@ int ref_mlfmm(int d, int n, const double* x, const double* lo,
     RadialKernel k = parse_kernel_spec(spec);
     BoxTree tree = build_tree(ps, leaf);
     LevelGrids grids =
-        make_level_grids(k, sigma, m, d, leaf, GridMode::shared, 10);
+        make_level_grids(k, sigma, m, d, leaf, g_mode, g_stencil);
     SumRequest req{k, sigma, &ps, std::vector<double>(w, w + n), m};
     double best = 1e300;
     SumResult r;
@@ -156,7 +179,7 @@ int ref_expansions(int d, int n, const double* x, const double* lo,
     RadialKernel k = parse_kernel_spec(spec);
     BoxTree tree = build_tree(ps, leaf);
     LevelGrids grids =
-        make_level_grids(k, sigma, m, d, leaf, GridMode::shared, 10);
+        make_level_grids(k, sigma, m, d, leaf, g_mode, g_stencil);
     auto mult = upsweep(tree, grids, ps, std::vector<double>(w, w + n));
     const LevelExpansions* src = &mult;
     LevelExpansions loc;

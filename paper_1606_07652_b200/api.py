@@ -245,18 +245,31 @@ class LevelGrids:
     interp: list = field(default_factory=list)
 
 
+def rescale_grid(grid: QuadratureGrid, s: float) -> QuadratureGrid:
+    """bandlimit.cpp:294-305: nodes / s, weights / s^d (sum w = (2 sigma/s)^d)."""
+    if not s > 0.0:
+        raise InvalidArgument("s must be positive")
+    return QuadratureGrid(grid.sigma / s, grid.m_per_dim, grid.d, grid.nodes / s,
+                          grid.weights / s ** grid.d)
+
+
 def make_level_grids(kernel: RadialKernel, sigma_leaf: float, m_leaf: int, d: int,
                      leaf_level: int, mode: GridMode = GridMode.shared,
                      stencil_k: int = 10) -> LevelGrids:
-    """mlfmm.cpp:112-142. Shared mode: every level reuses the leaf grid and C."""
+    """mlfmm.cpp:112-142. Shared mode: every level reuses the leaf grid and C.
+    Scaled mode: sigma_{l-1} = sigma_l / 2 and one C table per level; the GPU
+    plan builds the Lagrange transfers itself (stencil_k)."""
     if leaf_level < 2:
         raise InvalidArgument("leaf_level must be >= 2")
-    if mode != GridMode.shared:
-        raise DomainError("GridMode.scaled is not implemented on the GPU path")
     g = make_quadrature(sigma_leaf, m_leaf, d)
+    grids = [None] * (leaf_level + 1)
+    factors = [None] * (leaf_level + 1)
+    grids[leaf_level] = g
+    for l in range(leaf_level - 1, 1, -1):
+        grids[l] = grids[l + 1] if mode == GridMode.shared else rescale_grid(grids[l + 1], 2.0)
     f = translation_coefficients(kernel, g)
-    grids = [None, None] + [g] * (leaf_level - 1)
-    factors = [None, None] + [f] * (leaf_level - 1)
+    for l in range(2, leaf_level + 1):
+        factors[l] = f if mode == GridMode.shared else translation_coefficients(kernel, grids[l])
     return LevelGrids(mode, d, leaf_level, min(stencil_k, m_leaf), kernel, grids, factors)
 
 
@@ -298,7 +311,8 @@ class Plan:
 
     def __init__(self, ps: PointSet, leaf_level: int, kernel: RadialKernel, sigma: float,
                  m_per_dim: int, c_table: np.ndarray | None = None, nrhs: int = 1,
-                 device: int = -1, rank: int = 0, world: int = 1):
+                 device: int = -1, rank: int = 0, world: int = 1, grid_mode: int = 0,
+                 stencil_k: int = 10):
         self._h = ct.c_void_p()
         self._keep = []
         d = ps.d
@@ -316,8 +330,8 @@ class Plan:
         desc.sigma = sigma
         desc.m_per_dim = m_per_dim
         desc.leaf_level = leaf_level
-        desc.grid_mode = 0
-        desc.stencil_k = 10
+        desc.grid_mode = int(grid_mode)
+        desc.stencil_k = int(stencil_k)
         desc.nrhs = nrhs
         desc.device = device
         if c_table is not None:
@@ -415,8 +429,13 @@ def _plan_for(req: SumRequest, tree: BoxTree, grids: LevelGrids, nrhs: int) -> P
     plan = cache.get(key)
     if plan is None:
         g = grids.grids[tree.leaf_level]
-        plan = Plan(ps, tree.leaf_level, req.kernel, g.sigma, g.m_per_dim,
-                    c_table=grids.factors[tree.leaf_level].c_vals, nrhs=nrhs)
+        if grids.mode == GridMode.scaled:
+            ctab = np.concatenate([grids.factors[l].c_vals
+                                   for l in range(2, tree.leaf_level + 1)])
+        else:
+            ctab = grids.factors[tree.leaf_level].c_vals
+        plan = Plan(ps, tree.leaf_level, req.kernel, g.sigma, g.m_per_dim, c_table=ctab,
+                    nrhs=nrhs, grid_mode=int(grids.mode), stencil_k=grids.stencil_k)
         cache.clear()
         cache[key] = plan
     return plan

@@ -18,15 +18,18 @@ from oracle import pyoracle as po  # noqa: E402
 from paper_1606_07652_b200 import inputs as I  # noqa: E402
 
 
-def mlfmm_fixture(name, x, w, spec, sigma, m, leaf, with_direct=False):
-    v, st = po.ref_mlfmm(x, w, spec, sigma, m, leaf)
+def mlfmm_fixture(name, x, w, spec, sigma, m, leaf, with_direct=False, mode=0, stencil=10):
+    v, st = po.ref_mlfmm(x, w, spec, sigma, m, leaf, mode=mode, stencil=stencil)
     extra = {}
     if with_direct:
         dv, _ = po.ref_direct(x, w, spec)
         extra["direct"] = dv
+    if mode == 1:  # the reference's own per-level C tables (LevelGrids::factors)
+        extra["ctab"] = po.ref_level_c_tables(spec, sigma, m, x.shape[1], leaf, mode, stencil)
     np.savez_compressed(os.path.join(HERE, name + ".npz"), kind="mlfmm", x=x, w=w, spec=spec,
                         sigma=sigma, m=m, leaf=leaf, values=v, near_pairs=st["near_pairs"],
-                        far_work=st["far_work"], max_imag=st["max_imag_residual"], **extra)
+                        far_work=st["far_work"], max_imag=st["max_imag_residual"],
+                        grid_mode=mode, stencil_k=stencil, **extra)
     print(name, x.shape, st)
 
 
@@ -51,6 +54,18 @@ def main():
     x = I.generate_quasiuniform(1024, 1, 2026, 0.35)
     w = I.uniform_weights(1024, 99)
     mlfmm_fixture("imq_1d_ref", x, w, "imq:c=1", math.pi, 64, 5)
+    # GridMode::scaled (halved band per level, Lagrange transfers)
+    x = I.generate_quasiuniform(512, 1, 55, 0.4)
+    w = I.uniform_weights(512, 56)
+    mlfmm_fixture("scaled_gaussian_1d_ref", x, w, "gaussian:c=1", math.pi, 16, 5, mode=1,
+                  stencil=6)
+    x = I.uniform_points(1024, 2, 61)
+    w = I.uniform_weights(1024, 62)
+    mlfmm_fixture("scaled_imq_2d_ref", x, w, "imq:c=1", math.pi, 12, 4, mode=1, stencil=10)
+    x = I.uniform_points(600, 2, 63)
+    w = I.uniform_weights(600, 64)
+    mlfmm_fixture("scaled_mq_2d_global_stencil_ref", x, w, "mq:c=0.5", math.pi, 8, 3, mode=1,
+                  stencil=8)
 
 
 if __name__ == "__main__":

@@ -292,7 +292,68 @@ def test_golden_fixtures_match_oracle(oracle):
         g = np.load(f, allow_pickle=False)
         if str(g["kind"]) != "mlfmm":
             continue
+        mode = int(g["grid_mode"]) if "grid_mode" in g.files else 0
+        stencil = int(g["stencil_k"]) if "stencil_k" in g.files else 10
         v, st, _ = oracle.mlfmm(g["x"], g["w"], str(g["spec"]), float(g["sigma"]),
-                                int(g["m"]), int(g["leaf"]))
+                                int(g["m"]), int(g["leaf"]), mode=mode, stencil=stencil,
+                                c_table_in=g["ctab"].ravel() if "ctab" in g.files else None)
         assert rel_l2(v, g["values"]) <= 1e-14, f
         assert st["near_pairs"] == int(g["near_pairs"]) and st["far_work"] == int(g["far_work"])
+        assert abs(st["max_imag_residual"] - float(g["max_imag"])) <= \
+            1e-12 * max(1.0, float(g["max_imag"])), f
+
+
+# ---------------------------------------------------- GridMode::scaled
+@pytest.mark.parametrize("d,n,leaf,m,spec,stencil", [
+    (1, 200, 4, 16, "gaussian:c=1", 6), (1, 300, 5, 32, "imq:c=1", 10),
+    (2, 400, 3, 12, "imq:c=1", 4), (2, 500, 4, 16, "mq:c=0.5", 10),
+    (2, 300, 3, 8, "gaussian:c=4", 8)])
+def test_scaled_mode_matches_reference(oracle, d, n, leaf, m, spec, stencil):
+    """Oracle restatement of GridMode::scaled (per-level grids and C tables,
+    Lagrange M2M/L2L, mlfmm.cpp:39-197, 256-261, 331-337) against the
+    reference compiled from its own sources: same bits, same stats."""
+    if not oracle.ref_available():
+        pytest.skip("reference not built")
+    rng = np.random.default_rng(d * 100 + n)
+    x = rng.random((n, d))
+    w = rng.uniform(-1, 1, n)
+    rv, rs = oracle.ref_mlfmm(x, w, spec, math.pi, m, leaf, mode=1, stencil=stencil)
+    ov, os_, _ = oracle.mlfmm(x, w, spec, math.pi, m, leaf, mode=1, stencil=stencil)
+    assert rel_l2(ov, rv) <= 1e-14
+    assert os_["near_pairs"] == rs["near_pairs"] and os_["far_work"] == rs["far_work"]
+    assert abs(os_["max_imag_residual"] - rs["max_imag_residual"]) <= \
+        1e-12 * max(1.0, rs["max_imag_residual"])
+    # per-level C tables: the reference's factors[l] == the oracle's c_table(sigma_l)
+    ct = oracle.ref_level_c_tables(spec, math.pi, m, d, leaf, mode=1, stencil=stencil)
+    for l in range(2, leaf + 1):
+        sig = math.pi / 2 ** (leaf - l)
+        assert np.abs(ct[l - 2] - oracle.c_table(spec, sig, m, d)).max() <= \
+            1e-14 * np.abs(ct[l - 2]).max()
+
+
+def test_scaled_stage_expansions_match_reference(oracle):
+    if not oracle.ref_available():
+        pytest.skip("reference not built")
+    rng = np.random.default_rng(5)
+    x = rng.random((4000, 2))  # every box occupied (the reference also fills empty boxes)
+    w = rng.uniform(-1, 1, 4000)
+    for level in (2, 3, 4):
+        for kind in (0, 1):
+            a = oracle.expansions(x, w, "imq:c=1", math.pi, 12, 4, level, kind, mode=1, stencil=6)
+            b = oracle.ref_expansions(x, w, "imq:c=1", math.pi, 12, 4, level, kind, mode=1,
+                                      stencil=6)
+            assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max(), (level, kind)
+
+
+def test_scaled_grids_halve_the_band(oracle):
+    """test_mlfmm.cpp:113-140 on the Python mirror: sigma_l = sigma / 2^{L-l},
+    nodes and weights halve per level, stencil clamped to M."""
+    import paper_1606_07652_b200 as B
+    k = B.parse_kernel_spec("gaussian:c=1")
+    g = B.make_level_grids(k, math.pi, 16, 1, 4, B.GridMode.scaled, 6)
+    for l in (3, 2):
+        assert g.grids[l].sigma == pytest.approx(math.pi / (1 << (4 - l)))
+        assert np.allclose(g.grids[l].nodes, g.grids[l + 1].nodes / 2.0, rtol=1e-15, atol=0)
+        assert np.allclose(g.grids[l].weights, g.grids[l + 1].weights / 2.0, rtol=1e-15, atol=0)
+    h = B.make_level_grids(k, math.pi, 8, 1, 3, B.GridMode.scaled, 64)
+    assert h.stencil_k == 8

@@ -25,14 +25,16 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-def gpu_mlfmm(B, x, w, spec, sigma, m, leaf, lo=None, hi=None, c_table=None):
+def gpu_mlfmm(B, x, w, spec, sigma, m, leaf, lo=None, hi=None, c_table=None, grid_mode=0,
+              stencil_k=10):
     d = x.shape[1]
     dom = B.BoundingBox(tuple(lo) if lo is not None else (0.0,) * 3,
                         tuple(hi) if hi is not None else (1.0,) * 3)
     ps = B.PointSet(d, x, dom)
     w = np.asarray(w)
     plan = B.Plan(ps, leaf, B.parse_kernel_spec(spec), sigma, m, c_table=c_table,
-                  nrhs=1 if w.ndim == 1 else w.shape[0])
+                  nrhs=1 if w.ndim == 1 else w.shape[0], grid_mode=grid_mode,
+                  stencil_k=stencil_k)
     return plan.execute(w), plan
 
 
@@ -71,8 +73,13 @@ def test_golden_reference_fixtures(blfmm):
     assert files
     for f in files:
         g = np.load(f, allow_pickle=False)
+        mode = int(g["grid_mode"]) if "grid_mode" in g.files else 0
         res, _ = gpu_mlfmm(blfmm, g["x"], g["w"], str(g["spec"]), float(g["sigma"]),
-                           int(g["m"]), int(g["leaf"]))
+                           int(g["m"]), int(g["leaf"]), grid_mode=mode,
+                           stencil_k=int(g["stencil_k"]) if "stencil_k" in g.files else 10,
+                           c_table=g["ctab"].ravel() if "ctab" in g.files else None)
+        assert abs(res.stats.max_imag_residual - float(g["max_imag"])) <= \
+            1e-8 * max(1.0, float(g["max_imag"])), f
         assert rel_l2(res.values, g["values"]) <= TOL, (f, rel_l2(res.values, g["values"]))
         assert res.stats.near_pairs == int(g["near_pairs"])
         assert res.stats.far_work == int(g["far_work"])
@@ -368,3 +375,64 @@ def test_exchange_mode_assembles_to_full(blfmm, name, n, leaf):
             acc += out
         got = acc.cpu().numpy()[0]
         assert rel_l2(got, full) <= 1e-13, (world, rel_l2(got, full))
+
+
+# ------------------------------------------------------- GridMode::scaled
+def scaled_tables(B, spec, sigma, m, d, leaf):
+    k = B.parse_kernel_spec(spec)
+    g = B.make_level_grids(k, sigma, m, d, leaf, B.GridMode.scaled)
+    return np.concatenate([g.factors[l].c_vals for l in range(2, leaf + 1)])
+
+
+@pytest.mark.parametrize("d,n,leaf,m,spec,stencil", [
+    (1, 2000, 6, 16, "gaussian:c=1", 6), (2, 3000, 4, 12, "imq:c=1", 10),
+    (2, 4000, 5, 16, "mq:c=0.5", 4), (3, 3000, 3, 8, "imq:c=0.1", 6),
+    (3, 4000, 4, 12, "gaussian:c=8", 12)])
+def test_scaled_mode_matches_oracle(blfmm, oracle, d, n, leaf, m, spec, stencil):
+    """GridMode::scaled on the GPU (Lagrange M2M/L2L in shared memory, direct
+    interaction-list couple on per-level grids) against the oracle with the
+    same per-level C tables."""
+    x = I.uniform_points(n, d, 70 + d)
+    w = I.uniform_weights(n, 80 + d)
+    ctab = scaled_tables(blfmm, spec, math.pi, m, d, leaf)
+    res, plan = gpu_mlfmm(blfmm, x, w, spec, math.pi, m, leaf, c_table=ctab, grid_mode=1,
+                          stencil_k=stencil)
+    ov, ost, _ = oracle.mlfmm(x, w, spec, math.pi, m, leaf, c_table_in=ctab, mode=1,
+                              stencil=stencil)
+    assert rel_l2(res.values, ov) <= TOL, rel_l2(res.values, ov)
+    assert res.stats.near_pairs == ost["near_pairs"]
+    assert res.stats.far_work == ost["far_work"]
+    assert abs(res.stats.max_imag_residual - ost["max_imag_residual"]) <= \
+        1e-8 * max(1.0, ost["max_imag_residual"])
+    # the plan's own per-level tables (no caller C) give the same result
+    own, _ = gpu_mlfmm(blfmm, x, w, spec, math.pi, m, leaf, grid_mode=1, stencil_k=stencil)
+    assert rel_l2(own.values, ov) <= TOL
+
+
+@pytest.mark.parametrize("d,leaf,m", [(2, 4, 12), (3, 3, 8)])
+def test_scaled_stage_expansions_match_oracle(blfmm, oracle, d, leaf, m):
+    x = I.uniform_points(2500, d, 90 + d)
+    w = I.uniform_weights(2500, 95 + d)
+    spec = "imq:c=1"
+    ctab = scaled_tables(blfmm, spec, math.pi, m, d, leaf)
+    ps = blfmm.PointSet(d, x)
+    plan = blfmm.Plan(ps, leaf, blfmm.parse_kernel_spec(spec), math.pi, m, c_table=ctab,
+                      grid_mode=1, stencil_k=6)
+    plan.set_keep_couple(True)
+    plan.execute(w)
+    for level in range(2, leaf + 1):
+        for kind in (0, 1, 2):
+            a = plan.expansions(level, kind)
+            b = oracle.expansions(x, w, spec, math.pi, m, leaf, level, kind, c_table_in=ctab,
+                                  mode=1, stencil=6)
+            assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max(), (level, kind)
+
+
+def test_scaled_mode_validation(blfmm):
+    x = I.uniform_points(100, 3, 1)
+    ps = blfmm.PointSet(3, x)
+    k = blfmm.parse_kernel_spec("imq:c=1")
+    with pytest.raises(blfmm.DomainError):  # M^d too large for the shared-memory transfers
+        blfmm.Plan(ps, 3, k, math.pi, 20, grid_mode=1)
+    with pytest.raises(blfmm.DomainError):  # scaled grids are single-GPU
+        blfmm.Plan(ps, 3, k, math.pi, 8, grid_mode=1, rank=0, world=2)

@@ -1,1 +1,3 @@
-for f in 0 1; do BLFMM_FUSE_NEAR_M2M=$f python tools/time_step.py --tag fuse$f 2>&1 | tail -1; done
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3
+python tools/time_step.py --tag shared --steps 10
+python tools/time_step.py --tag scaled10 --scaled 10 --steps 3
