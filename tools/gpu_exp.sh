@@ -1,3 +1,1 @@
-timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3
-python tools/time_step.py --tag shared --steps 10
-python tools/time_step.py --tag scaled10 --scaled 10 --steps 3
+for b in 3 4; do BLFMM_COUPLE_MINB=$b python tools/run_steps.py --scaled 10 --steps 2 2>&1 | tail -1 | sed "s/^/minb$b /"; done > gpurun_out/log.txt 2>&1

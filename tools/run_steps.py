@@ -20,12 +20,14 @@ def main():
     ap.add_argument("--workload", default="P3")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--scaled", type=int, default=0, help="GridMode::scaled with this stencil")
     args = ap.parse_args()
     W = I.WORKLOADS[args.workload]
     x, w = W.make(args.n)
     n = x.shape[0]
     plan = B.Plan(B.PointSet(W.d, x), W.leaf, B.parse_kernel_spec(W.kernel), W.sigma, W.m,
-                  nrhs=W.nrhs)
+                  nrhs=W.nrhs, grid_mode=1 if args.scaled else 0,
+                  stencil_k=args.scaled if args.scaled else 10)
     lam = torch.from_numpy(np.ascontiguousarray(w.reshape(W.nrhs, n))).cuda()
     out = torch.empty_like(lam)
     s = torch.cuda.Stream()
