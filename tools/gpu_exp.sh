@@ -1,1 +1,2 @@
-for b in 3 4; do BLFMM_COUPLE_MINB=$b python tools/run_steps.py --scaled 10 --steps 2 2>&1 | tail -1 | sed "s/^/minb$b /"; done > gpurun_out/log.txt 2>&1
+for v in "1 4" "6 3" "6 4" "6 5"; do set -- $v; BLFMM_COUPLE_VARIANT=$1 BLFMM_COUPLE_MINB=$2 python tools/run_steps.py --steps 2 2>&1 | tail -1 | sed "s/^/v$1 minb$2 /"; done > gpurun_out/log.txt 2>&1
+BLFMM_COUPLE_VARIANT=6 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2 >> gpurun_out/log.txt
