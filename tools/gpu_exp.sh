@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_cli.py -x -q 2>&1 | tail -15 > gpurun_out/log.txt
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -2 > gpurun_out/log.txt
