@@ -436,3 +436,27 @@ def test_scaled_mode_validation(blfmm):
         blfmm.Plan(ps, 3, k, math.pi, 20, grid_mode=1)
     with pytest.raises(blfmm.DomainError):  # scaled grids are single-GPU
         blfmm.Plan(ps, 3, k, math.pi, 8, grid_mode=1, rank=0, world=2)
+
+
+def test_graph_replay_matches_direct_launch(blfmm, monkeypatch):
+    """execute_device captures the launch sequence into a CUDA graph on the
+    second use of a (lambda, out) pointer pair and replays it afterwards; the
+    replayed matvec equals a plan that launches directly, bit for bit."""
+    import torch
+    W = I.WORKLOADS["P3"]
+    x, w = W.make(20000)
+    k = blfmm.parse_kernel_spec(W.kernel)
+    ps = blfmm.PointSet(W.d, x)
+    lam = torch.from_numpy(np.ascontiguousarray(w.reshape(1, -1))).cuda()
+    outs = []
+    for graphs in ("1", "0"):
+        monkeypatch.setenv("BLFMM_GRAPHS", graphs)
+        plan = blfmm.Plan(ps, 4, k, W.sigma, W.m)
+        out = torch.empty_like(lam)
+        for _ in range(4):  # direct, capture + replay, replay, replay
+            out.zero_()
+            plan.execute_device(lam.data_ptr(), out.data_ptr())
+            torch.cuda.synchronize()
+            outs.append(out.cpu().numpy().copy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])

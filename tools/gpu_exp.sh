@@ -1,2 +1,1 @@
-for v in 1 8; do BLFMM_COUPLE_VARIANT=$v python tools/run_steps.py --steps 2 2>&1 | tail -1 | sed "s/^/v$v /"; done > gpurun_out/log.txt 2>&1
-BLFMM_COUPLE_VARIANT=8 timeout 900 python -m pytest tests -m gpu -x -q -k "P3 or stage or golden or exchange" 2>&1 | tail -2 >> gpurun_out/log.txt
+timeout 900 python -m pytest tests -m gpu -x -q -k "graph_replay" 2>&1 | tail -3 > gpurun_out/log.txt
