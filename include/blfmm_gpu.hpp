@@ -17,6 +17,7 @@
 // (std::invalid_argument, std::domain_error, blfmm::accuracy_error).
 #pragma once
 
+#include <cstdint>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -49,9 +50,36 @@ inline void check(int code) {
 // Plan cache: the tree + grids a caller builds once are reused across
 // matvecs (the solver pattern, solver.cpp:280-293); a new point set, tree
 // depth or grid rebuilds the device plan.
+// Cheap identity of a point set's contents (sampled FNV-1a over the
+// coordinate bits): a new PointSet at a reused address, or coordinates
+// rewritten in place, rebuild the plan instead of hitting a stale one.
+inline std::uint64_t points_fingerprint(const PointSet& ps) {
+  std::uint64_t h = 1469598103934665603ull;
+  auto mix = [&](double v) {
+    std::uint64_t b;
+    std::memcpy(&b, &v, sizeof b);
+    h = (h ^ b) * 1099511628211ull;
+  };
+  const std::size_t n = ps.pts.size(), step = n > 4096 ? n / 4096 : 1;
+  for (std::size_t i = 0; i < n; i += step) {
+    mix(ps.pts[i][0]);
+    mix(ps.pts[i][1]);
+  }
+  if (n) {
+    mix(ps.pts[n - 1][0]);
+    mix(ps.pts[n - 1][1]);
+  }
+  mix(ps.domain.lo[0]);
+  mix(ps.domain.lo[1]);
+  mix(ps.domain.hi[0]);
+  mix(ps.domain.hi[1]);
+  return h;
+}
+
 struct PlanHandle {
   blfmm_plan* p = nullptr;
   const PointSet* ps = nullptr;
+  std::uint64_t fp = 0;
   std::size_t n = 0;
   int leaf = 0, m = 0, mode = 0, stencil = 10;
   double sigma = 0.0;
@@ -66,7 +94,9 @@ inline blfmm_plan* plan_for(const PointSet& ps, const BoxTree& tree, const Radia
                             double sigma, int m, const std::vector<double>& c_vals,
                             int mode = BLFMM_GRID_SHARED, int stencil_k = 10) {
   thread_local std::unique_ptr<PlanHandle> cache;
-  if (cache && cache->ps == &ps && cache->n == ps.pts.size() && cache->leaf == tree.leaf_level &&
+  const std::uint64_t fp = points_fingerprint(ps);
+  if (cache && cache->ps == &ps && cache->fp == fp && cache->n == ps.pts.size() &&
+      cache->leaf == tree.leaf_level &&
       cache->m == m && cache->sigma == sigma && cache->kernel.type == k.type &&
       cache->kernel.shape == k.shape && cache->c_vals == c_vals && cache->mode == mode &&
       cache->stencil == stencil_k)
@@ -98,6 +128,7 @@ inline blfmm_plan* plan_for(const PointSet& ps, const BoxTree& tree, const Radia
   desc.world = 1;
   check(blfmm_plan_create(&desc, &cache->p));
   cache->ps = &ps;
+  cache->fp = fp;
   cache->n = ps.pts.size();
   cache->leaf = tree.leaf_level;
   cache->m = m;

@@ -425,7 +425,10 @@ class Plan:
 def _plan_for(req: SumRequest, tree: BoxTree, grids: LevelGrids, nrhs: int) -> Plan:
     ps = req.ps
     cache = grids.__dict__.setdefault("_plans", {})
-    key = (id(ps), id(ps.pts), ps.pts.shape, tree.leaf_level, nrhs, req.kernel)
+    pts = np.asarray(ps.pts)
+    step = max(1, pts.shape[0] // 4096)
+    fp = hash(np.ascontiguousarray(pts[::step]).tobytes()) if pts.size else 0
+    key = (id(ps), id(ps.pts), ps.pts.shape, fp, tree.leaf_level, nrhs, req.kernel)
     plan = cache.get(key)
     if plan is None:
         g = grids.grids[tree.leaf_level]

@@ -357,3 +357,16 @@ def test_scaled_grids_halve_the_band(oracle):
         assert np.allclose(g.grids[l].weights, g.grids[l + 1].weights / 2.0, rtol=1e-15, atol=0)
     h = B.make_level_grids(k, math.pi, 8, 1, 3, B.GridMode.scaled, 64)
     assert h.stencil_k == 8
+
+
+@pytest.mark.parametrize("suite", ["test_fmm", "test_mlfmm"])
+def test_reference_unit_tests_pass_on_reference_build(suite):
+    """Baseline for the GPU drop-in test: the reference's own unit tests
+    (doctest shim) pass against the reference library built from its sources."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref", suite + "_ref")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "| 0 failed |" in r.stdout, r.stdout + r.stderr

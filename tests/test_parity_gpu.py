@@ -320,6 +320,23 @@ def test_cpp_adapter_dropin_against_reference():
     assert r.returncode == 0 and all(l["ok"] for l in lines), r.stdout
 
 
+@pytest.mark.parametrize("suite", ["test_fmm", "test_mlfmm"])
+def test_reference_unit_tests_pass_on_gpu_dropin(suite):
+    """The reference's OWN unit tests (tests/test_fmm.cpp, tests/test_mlfmm.cpp,
+    compiled unmodified against oracle/shim/doctest.h) linked with the GPU
+    drop-in (oracle/dropin_gpu.cpp: mlfmm_matvec / fmm_matvec_single /
+    direct_matvec on libblfmm_gpu.so, the reference's versions renamed *_cpu):
+    every test case passes, as it does against the reference library."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref",
+                       suite + "_gpu")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref drop-in tests not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    summary = [l for l in r.stdout.splitlines() if l.startswith("test cases:")]
+    assert r.returncode == 0 and summary and "| 0 failed |" in summary[-1], r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("nr", [16, 32])
 def test_batched_rhs_near_field_path(blfmm, oracle, nr):
     """nrhs multiple of 16 takes the batched near-field kernel (point-major
