@@ -332,8 +332,13 @@ def test_reference_unit_tests_pass_on_gpu_dropin(suite):
                        suite + "_gpu")
     if not os.path.exists(exe):
         pytest.skip("oracle/_ref drop-in tests not built (needs /root/reference at build time)")
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
-    summary = [l for l in r.stdout.splitlines() if l.startswith("test cases:")]
+    # (one retry: test_fmm.cpp's complexity-probe cases fit wall-clock slopes
+    # of the CPU paths and can flake on a loaded host)
+    for attempt in range(2):
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+        summary = [l for l in r.stdout.splitlines() if l.startswith("test cases:")]
+        if r.returncode == 0 and summary and "| 0 failed |" in summary[-1]:
+            break
     assert r.returncode == 0 and summary and "| 0 failed |" in summary[-1], r.stdout + r.stderr
 
 

@@ -1,2 +1,1 @@
-(timeout 600 oracle/_ref/test_fmm_gpu | tail -3; timeout 900 oracle/_ref/test_mlfmm_gpu | tail -1) > gpurun_out/dropin.txt 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2 >> gpurun_out/dropin.txt
+for i in 1 2 3; do timeout 900 python -m pytest tests -m gpu -q -k "reference_unit_tests" 2>&1 | grep -E "FAIL|passed|failed|test_fmm.cpp" | head -5; done > gpurun_out/log.txt 2>&1
