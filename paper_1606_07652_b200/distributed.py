@@ -27,10 +27,12 @@ from .api import InvalidArgument, Plan, PointSet, RadialKernel
 
 
 def leaf_cost(npts: np.ndarray, nsrc: np.ndarray, K: int) -> np.ndarray:
-    """Per-leaf cost model used by the plan (blfmm.cu, plan_build_tree):
-    near pairs x 20 + points x 2K (P2M/L2P) + 100 K (translations)."""
+    """Per-leaf cost model used by the plan (blfmm.cu, plan_build_tree), in
+    units of one near-field pair and calibrated on the P3 kernels: near pairs
+    + 1.1 K per point (P2M / L2P) + 19 K per leaf (translations), with K the
+    stored nodes per expansion (blfmm_plan_info.stored_nodes)."""
     npts = np.asarray(npts, dtype=np.float64)
-    return 20.0 * npts * np.asarray(nsrc, dtype=np.float64) + 2.0 * npts * K + 100.0 * K
+    return npts * np.asarray(nsrc, dtype=np.float64) + 1.1 * npts * K + 19.0 * K
 
 
 def partition(cost: np.ndarray, world: int) -> np.ndarray:
