@@ -368,5 +368,10 @@ def test_reference_unit_tests_pass_on_reference_build(suite):
     exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref", suite + "_ref")
     if not os.path.exists(exe):
         pytest.skip("oracle/_ref not built")
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    # (retries: test_fmm.cpp's complexity-probe cases fit wall-clock slopes and
+    # can flake on a loaded host)
+    for attempt in range(3):
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+        if r.returncode == 0 and "| 0 failed |" in r.stdout:
+            break
     assert r.returncode == 0 and "| 0 failed |" in r.stdout, r.stdout + r.stderr
