@@ -281,8 +281,9 @@ def test_full_size_p3_properties(blfmm):
 @pytest.mark.parametrize("name,n,leaf", [("P3", 60000, 4), ("P4", 50000, 5), ("P1", 4096, 3)])
 def test_sharded_plans_assemble_to_full(blfmm, name, n, leaf):
     """Morton-range sharding: the owned outputs of world plans (one per rank,
-    here all on one GPU, no collective) sum to the single-plan matvec exactly,
-    and the owned near-pair counts add up."""
+    here all on one GPU, no collective) sum to the single-plan matvec (up to
+    the re-association of split near-field items), and the owned near-pair
+    counts add up."""
     W = I.WORKLOADS[name]
     x, w = W.make(n)
     k = blfmm.parse_kernel_spec(W.kernel)
@@ -299,7 +300,9 @@ def test_sharded_plans_assemble_to_full(blfmm, name, n, leaf):
             pairs += r.stats.near_pairs
             inf = pl.info()
             owned.append(inf.owned_end - inf.owned_begin)
-        assert np.array_equal(acc, full.values), world
+        # bit-identical unless near-field items were split on the sharded plans
+        # (3 partial sums re-associated): rounding level
+        assert np.abs(acc - full.values).max() <= 1e-14 * np.abs(full.values).max(), world
         assert pairs == full.stats.near_pairs
         assert sum(owned) == n
 
