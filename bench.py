@@ -141,7 +141,12 @@ def far_bytes(info, K, nrhs):
     B = [info.boxes[l] for l in range(L + 1)]
     cb = 16 * K * nrhs
     m2m = sum((B[l] + B[l - 1]) * cb for l in range(2, L + 1))
-    m2l = sum(2 * B[l] * cb + (B[l - 1] * cb if l >= 2 else 0) for l in range(1, L + 1))
+    if getattr(info, "telescoped", 0):
+        # telescoped: k_root reads V_1 and writes C V_0; the leaf couple reads
+        # V_L once and writes L_L (no intermediate G levels)
+        m2l = (B[1] + 1) * cb + 2 * B[L] * cb
+    else:
+        m2l = sum(2 * B[l] * cb + (B[l - 1] * cb if l >= 2 else 0) for l in range(1, L + 1))
     return m2m, m2l
 
 

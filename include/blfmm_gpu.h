@@ -108,6 +108,8 @@ typedef struct blfmm_plan_info {
   long long device_bytes;
   long long stored_nodes;   /* complex coefficients stored per expansion: K, or
                                the Hermitian half spectrum (3-D, M = 16: 2528) */
+  int telescoped;           /* 1: execute evaluates G_L from the root multipole
+                               (leaf-level couple only) */
 } blfmm_plan_info;
 
 /* Per-stage device times of the last execute (CUDA events on the launch

@@ -51,7 +51,7 @@ class PlanInfo(ct.Structure):
         ("far_work_single", ct.c_longlong), ("il_pairs", ct.c_longlong),
         ("owned_begin", ct.c_longlong), ("owned_end", ct.c_longlong),
         ("plan_seconds", ct.c_double), ("device_bytes", ct.c_longlong),
-        ("stored_nodes", ct.c_longlong),
+        ("stored_nodes", ct.c_longlong), ("telescoped", ct.c_int),
     ]
 
 

@@ -485,3 +485,30 @@ def test_graph_replay_matches_direct_launch(blfmm, monkeypatch):
             outs.append(out.cpu().numpy().copy())
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("name,n,leaf", [("P3", 40000, 4), ("P2p", 20000, 4), ("P5", 8192, 3)])
+def test_telescoped_equals_level_sweep(blfmm, oracle, name, n, leaf, monkeypatch):
+    """Shared grids make G_l a pure shift of G_1 = C V_0:
+    execute evaluates the leaf locals from the root multipole and skips the
+    level 1..L-1 couple launches. It equals the level-by-level G recursion to
+    rounding and the oracle to the north-star bar; stats are unchanged."""
+    W = I.WORKLOADS[name]
+    x, w = W.make(n)
+    if w.ndim == 2:
+        w = w[:16]
+    res = {}
+    for tv in ("0", "1"):
+        monkeypatch.setenv("BLFMM_TELESCOPE", tv)
+        r, plan = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
+        assert plan.info().telescoped == int(tv)
+        res[tv] = r
+    a, b = res["1"], res["0"]
+    assert rel_l2(a.values, b.values) <= 1e-13, rel_l2(a.values, b.values)
+    assert a.stats.near_pairs == b.stats.near_pairs and a.stats.far_work == b.stats.far_work
+    assert abs(a.stats.max_imag_residual - b.stats.max_imag_residual) <= \
+        1e-10 * max(1.0, b.stats.max_imag_residual)
+    ctab = blfmm.translation_coefficients(blfmm.parse_kernel_spec(W.kernel),
+                                          blfmm.make_quadrature(W.sigma, W.m, W.d)).c_vals
+    ov, _, _ = oracle.mlfmm(x, w, W.kernel, W.sigma, W.m, leaf, c_table_in=ctab)
+    assert rel_l2(a.values, ov) <= TOL
