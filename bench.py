@@ -289,17 +289,48 @@ def run_ours(args, W, world, rank, local):
     stage = {k_: {"ms": round(v[0], 4), "launches": v[1]} for k_, v in acc.items()}
     top = max(acc.items(), key=lambda kv: kv[1][0])[0]
     hbm_peak = pk.get("hbm_gbs", 6650.0)
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s"
+    fp = fp64_peak() or {}
+    dmma_peak, dfma_peak = fp.get("dmma_tflops", 37.2), fp.get("dfma_tflops", 37.2)
+    fp_src = ("profiles/fp64_peak.json (measured on B200 by tools/fp64_peak.cu; "
+              "MEASURED_PEAKS.json has no FP64 figure)" if fp else "nominal 37.2 TFLOP/s")
+    L = info.leaf_level
+    Bx = [info.boxes[l] for l in range(L + 1)]
+    cb = 16 * info.stored_nodes * nrhs
+    # algorithmic work per stage: P2M / L2P one
+    # complex MAC (8 flops) per point and grid node of the full K = M^d grid;
+    # M2M (levels L-1 -> 1, the leaf level is fused into P2M) and the couple
+    # bytes from the stored expansions; near field F_k flops per pair
+    near_fk = {"imq": 19, "mq": 16, "gaussian": 15}.get(W.kernel.split(":")[0], 16)
+    work = {
+        "p2m": ("k_p2m", "tensor", 8.0 * n * K * nrhs, "TFLOP/s", dmma_peak, fp_src),
+        "m2m": ("k_m2m", "hbm", float(sum((Bx[l] + Bx[l - 1]) * cb for l in range(2, L))),
+                "GB/s", hbm_peak, hbm_src),
+        "m2l_l2l": ("k_couple", "hbm", float(m2l_b), "GB/s", hbm_peak, hbm_src),
+        "l2p": ("k_l2p", "tensor", 8.0 * n * K * nrhs, "TFLOP/s", dmma_peak, fp_src),
+        "near": ("k_near", "fp64", float(near_fk) * info.near_pairs * nrhs, "TFLOP/s",
+                 dfma_peak, fp_src),
+    }
+    stage_roof = {}
+    for name, (kern, bound, amount, unit, peak_v, src) in work.items():
+        t_ms = acc.get(name, [0, 0])[0]
+        if t_ms <= 0 or amount <= 0:
+            continue
+        ach = amount / (t_ms / 1e3) / (1e9 if unit == "GB/s" else 1e12)
+        stage_roof[name] = {"kernel": kern + "*", "bound": bound, "achieved": round(ach, 2),
+                            "peak": peak_v, "unit": unit, "frac": round(ach / peak_v, 4),
+                            "traffic": load_traffic(kern),
+                            ("algorithmic_bytes" if unit == "GB/s" else "algorithmic_flops"): amount,
+                            "peak_source": src, "ms": round(t_ms, 4)}
     roof = None
+    if top in stage_roof:
+        roof = dict(stage_roof[top], dominant_stage=top)
+    elif "m2l_l2l" in stage_roof:
+        roof = dict(stage_roof["m2l_l2l"], dominant_stage=top)
     m2l_ms = acc.get("m2l_l2l", [0, 0])[0]
-    if m2l_ms > 0:
-        ach = m2l_b / (m2l_ms / 1e3) / 1e9
-        roof = {"kernel": "k_couple* (M2L + fused L2L)", "bound": "hbm", "achieved": round(ach, 1),
-                "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
-                "traffic": load_traffic("k_couple"),
-                "algorithmic_bytes": m2l_b,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s",
-                "dominant_stage": top,
-                "reference_equiv_tflops": round(8.0 * K * nrhs * info.il_pairs / (m2l_ms / 1e3) / 1e12, 3)}
+    if roof is not None and m2l_ms > 0:
+        roof["couple_reference_equiv_tflops"] = round(
+            8.0 * K * nrhs * info.il_pairs / (m2l_ms / 1e3) / 1e12, 3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -322,6 +353,7 @@ def run_ours(args, W, world, rank, local):
         "gpu_launches": launches * args.steps,
         "stages_ms": stage,
         "roofline": roof,
+        "stage_rooflines": stage_roof,
         "plan_seconds": plan_s,
         "parity": {"rel_l2_vs_gpu_direct_1024_targets": rel_direct,
                    "note": "informational (band-limited far field vs plain kernel); "
@@ -329,12 +361,11 @@ def run_ours(args, W, world, rank, local):
         "stats": {"near_pairs": info.near_pairs, "far_work": info.far_work,
                   "il_pairs_nonempty": info.il_pairs},
     }
-    fp = fp64_peak()
     near_ms = acc.get("near", [0, 0])[0]
-    if fp and near_ms > 0:
+    if near_ms > 0:
         line["near_field_fp64"] = {"pairs": info.near_pairs, "ms": near_ms,
                                    "pairs_per_s": info.near_pairs * nrhs / (near_ms / 1e3),
-                                   "peak_tflops": fp.get("dfma_tflops")}
+                                   "flops_per_pair": near_fk, "peak_tflops": dfma_peak}
     return line, clk.summary()
 
 
