@@ -11,9 +11,12 @@ supports are disjoint, so the sum is the matvec bit for bit.
 Exchange mode (leaf level >= 3, the default here): the upsweep is partitioned
 as well. Each rank runs P2M on its leaves plus a two-leaf halo, keeps complete
 multipoles at levels L and L-1 where its downsweep reads them, and writes
-partial multipoles of levels 1..L-2 (its own leaves only) into an exchange
+partial multipoles of the coarse levels (its own leaves only) into an exchange
 buffer; one NCCL all-reduce of that buffer is the upper-level expansion
-exchange, after which the downsweep runs. Without exchange mode
+exchange, after which the downsweep runs. With the telescoped 3-D downsweep
+(blfmm_plan_info.telescoped) the leaf locals need only the root multipole, so
+the buffer holds level 1 alone (8 expansions, 0.3 MB for P3); otherwise levels
+1..L-2. Without exchange mode
 (blfmm_execute on a world > 1 plan) the upsweep is replicated instead.
 """
 from __future__ import annotations

@@ -382,6 +382,9 @@ def test_exchange_mode_assembles_to_full(blfmm, name, n, leaf):
             pl = blfmm.Plan(ps, leaf, k, W.sigma, W.m, rank=rank, world=world)
             nx = pl.exchange_size()
             assert nx > 0
+            inf = pl.info()
+            if inf.telescoped:  # only the 8 level-1 multipoles (+ zero box) are exchanged
+                assert nx == 2 * (inf.boxes[1] + 1) * inf.stored_nodes, nx
             b = torch.zeros(nx, dtype=torch.float64, device="cuda")
             pl.bind_exchange(b.data_ptr())
             plans.append(pl)
