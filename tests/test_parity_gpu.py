@@ -515,3 +515,24 @@ def test_telescoped_equals_level_sweep(blfmm, oracle, name, n, leaf, monkeypatch
                                           blfmm.make_quadrature(W.sigma, W.m, W.d)).c_vals
     ov, _, _ = oracle.mlfmm(x, w, W.kernel, W.sigma, W.m, leaf, c_table_in=ctab)
     assert rel_l2(a.values, ov) <= TOL
+
+
+@pytest.mark.parametrize("env", [{"BLFMM_NEAR_SYM": "0"}, {"BLFMM_NEAR_PERSIST": "0"},
+                                 {"BLFMM_NEAR_SYM": "8", "BLFMM_NEAR_PERSIST": "2"}])
+def test_near_field_schedules_agree(blfmm, oracle, env, monkeypatch):
+    """The symmetric pair kernel (phi once per unordered pair of large
+    neighbouring leaves, per-neighbour planes), the persistent queue and the
+    one-sided kernels are the same near field: every configuration equals the
+    default one to rounding, and repeated executes are bit-identical (fixed
+    summation order, no atomics on values)."""
+    W = I.WORKLOADS["P3"]
+    x, w = W.make(60000)
+    leaf = 4  # 4096 leaves, ~15 points each: sym, one-sided and G-split items all occur
+    base, plan = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
+    again = plan.execute(w)
+    assert np.array_equal(base.values, again.values)
+    for k_, v in env.items():
+        monkeypatch.setenv(k_, v)
+    alt, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
+    assert rel_l2(alt.values, base.values) <= 1e-13, rel_l2(alt.values, base.values)
+    assert alt.stats.near_pairs == base.stats.near_pairs
