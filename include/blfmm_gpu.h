@@ -181,8 +181,10 @@ int blfmm_plan_owned_points(const blfmm_plan* plan, long long* idx);
 /* Exchange mode (world > 1, leaf level >= 3): the upsweep is partitioned too.
  * Each rank runs P2M on its leaves plus a two-leaf halo (complete multipoles
  * at levels L and L-1 where its downsweep reads them) and writes PARTIAL
- * multipoles of levels 1..L-2 (own leaves only, disjoint across ranks) into a
- * caller-bound device buffer of blfmm_plan_exchange_size doubles. The caller
+ * coarse multipoles (own leaves only, disjoint across ranks) into a
+ * caller-bound device buffer of blfmm_plan_exchange_size doubles: level 1
+ * only when blfmm_plan_info.telescoped (3-D: the leaf locals need just the
+ * root multipole; 0.3 MB for P3), levels 1..L-2 otherwise. The caller
  * all-reduces (sum) that buffer across ranks — the upper-level expansion
  * exchange over NCCL / NVLink — between the two halves:
  *   blfmm_execute_upsweep -> all-reduce(buffer) -> blfmm_execute_downsweep
