@@ -339,7 +339,7 @@ def run_ours(args, W, world, rank, local):
                    "sigma": W.sigma, "m_per_dim": W.m, "K": K, "leaf_level": W.leaf,
                    "points": W.points, "grid_mode": "shared",
                    "parallelism": (f"morton-range x{world} (halo P2M + NCCL all-reduce of "
-                                   f"levels 1..L-2 multipoles + all-reduce of u)")
+                                   f"level-1 multipoles (telescoped) + all-reduce of u)")
                                   if world > 1 else "single",
                    "l2": "per-step working set (expansions %.1f GB) >> 126 MB L2" %
                          (info.device_bytes / 1e9),
