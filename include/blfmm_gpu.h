@@ -139,12 +139,16 @@ int blfmm_plan_get_info(const blfmm_plan* plan, blfmm_plan_info* info);
 
 /* One matvec with HOST buffers: lambda [nrhs][n] (rhs-major, caller point
  * order), out [nrhs][n]. H2D / D2H copies are part of the call. stream may be
- * NULL (the plan's own stream). Synchronises before returning. */
+ * NULL (the plan's own stream). Synchronises before returning.
+ * stats may be NULL: SumResult's stats (fmm.hpp:10-14) are then not produced,
+ * and the max|Im| diagnostic of the far field (mlfmm.cpp:342-357) is not
+ * evaluated (the half-spectrum L2P skips its imaginary-residual GEMM); out is
+ * identical either way. The reference always fills them. */
 int blfmm_execute(blfmm_plan* plan, const double* lambda, double* out,
                   blfmm_stats* stats, void* stream);
 
 /* Same with DEVICE buffers (no copies, no host synchronisation; stats may be
- * NULL to avoid the D2H read of max_imag_residual). The work is ordered after
+ * NULL to skip max_imag_residual and its D2H read, as above). The work is ordered after
  * and before `stream` (NULL = the legacy default stream). */
 int blfmm_execute_device(blfmm_plan* plan, const double* d_lambda,
                          double* d_out, blfmm_stats* stats, void* stream);

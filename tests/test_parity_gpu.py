@@ -536,3 +536,56 @@ def test_near_field_schedules_agree(blfmm, oracle, env, monkeypatch):
     alt, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
     assert rel_l2(alt.values, base.values) <= 1e-13, rel_l2(alt.values, base.values)
     assert alt.stats.near_pairs == base.stats.near_pairs
+
+
+def test_split_symmetric_items_bit_identical(blfmm, monkeypatch):
+    """Symmetric pair items with more than 96 targets run as 96-target chunk
+    items (one warp each) whose source-side partials are summed in chunk
+    order by k_sym_fix: the same operations in the same order as one warp's
+    sequential passes, so the result is bit-identical to the unsplit queue."""
+    W = I.WORKLOADS["P3"]
+    x, w = W.make(60000)
+    leaf = 4
+    counts = np.bincount(blfmm_leaf_ids(x, leaf), minlength=8 ** leaf)
+    assert counts.max() > 96  # the split path is exercised
+    monkeypatch.setenv("BLFMM_SYM_SPLIT", "1")
+    base, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
+    monkeypatch.setenv("BLFMM_SYM_SPLIT", "0")
+    alt, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
+    assert np.array_equal(alt.values, base.values)
+
+
+def blfmm_leaf_ids(x, leaf):
+    """Row-major leaf ids with the reference's clamp binning (geometry.cpp:254-262)."""
+    n = 1 << leaf
+    c = np.clip((x * n).astype(np.int64), 0, n - 1)
+    return (c[:, 0] * n + c[:, 1]) * n + c[:, 2]
+
+
+def test_stats_request_only_adds_the_imag_residual(blfmm):
+    """Without a stats pointer the half-spectrum L2P skips its D-weighted
+    imaginary GEMM (max|Im| is not produced); u is bit-identical to a call
+    that requests the stats, alternating calls reuse the right CUDA graph,
+    and the residual returned with stats is unchanged."""
+    import torch
+    W = I.WORKLOADS["P3"]
+    x, w = W.make(20000)
+    k = blfmm.parse_kernel_spec(W.kernel)
+    plan = blfmm.Plan(blfmm.PointSet(W.d, x), 4, k, W.sigma, W.m)
+    assert plan.info().stored_nodes < plan.info().K  # half spectrum path
+    lam = torch.from_numpy(np.ascontiguousarray(w.reshape(1, -1))).cuda()
+    out = torch.empty_like(lam)
+    vals, res = [], []
+    for it in range(6):  # direct, capture, replay for each flag, interleaved
+        out.zero_()
+        st = plan.execute_device(lam.data_ptr(), out.data_ptr(), stats=bool(it % 2))
+        torch.cuda.synchronize()
+        vals.append(out.cpu().numpy().copy())
+        if st is not None:
+            res.append(st.max_imag_residual)
+    for v in vals[1:]:
+        assert np.array_equal(v, vals[0])
+    ref = plan.execute(w)
+    assert res[0] > 0 and all(r == res[0] for r in res)
+    assert ref.stats.max_imag_residual == res[0]
+    assert np.array_equal(ref.values, vals[0][0])
