@@ -518,7 +518,8 @@ def test_telescoped_equals_level_sweep(blfmm, oracle, name, n, leaf, monkeypatch
 
 
 @pytest.mark.parametrize("env", [{"BLFMM_NEAR_SYM": "0"}, {"BLFMM_NEAR_PERSIST": "0"},
-                                 {"BLFMM_NEAR_SYM": "8", "BLFMM_NEAR_PERSIST": "2"}])
+                                 {"BLFMM_NEAR_SYM": "8", "BLFMM_NEAR_PERSIST": "2"},
+                                 {"BLFMM_NEAR_STAGE": "0"}])
 def test_near_field_schedules_agree(blfmm, oracle, env, monkeypatch):
     """The symmetric pair kernel (phi once per unordered pair of large
     neighbouring leaves, per-neighbour planes), the persistent queue and the
