@@ -18,6 +18,6 @@ python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain2.log 2
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu2.log 2>&1
 python tools/time_step.py --workload P3 --steps 2 > gpurun_out/plain3.log 2>&1 && \
   ncu --set full --clock-control none --import-source on \
-      -k regex:"k_couple3|k_near_sym|k_near_warp2|k_l2p_h16S|k_p2m_m2m" -c 5 -o gpurun_out/prof_full \
+      -k regex:"k_couple3|k_near_all|k_l2p_h16S|k_p2m_m2m" -c 4 -o gpurun_out/prof_full \
       python tools/time_step.py --workload P3 --steps 2 > gpurun_out/ncu3.log 2>&1
 echo done > gpurun_out/evidence_done.txt
