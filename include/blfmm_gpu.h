@@ -18,6 +18,14 @@
  *                         const BoxTree&)                       include/blfmm/fmm.hpp:55
  *   blfmm_direct        SumResult direct_matvec(kernel, ps, weights,
  *                         use_bandlimited=false, ...)           include/blfmm/fmm.hpp:33-36
+ *   blfmm_direct_bandlimited  direct_matvec(kernel, ps, weights,
+ *                         use_bandlimited=true, sigma, refinement)  include/blfmm/fmm.hpp:33-36
+ *                       and direct_matvec_hybrid(kernel, ps, tree, weights,
+ *                         sigma, refinement)                    include/blfmm/fmm.hpp:40-43
+ *   blfmm_eval_bandlimited  eval_bandlimited(k, sigma, x, d, refinement)
+ *                                                               include/blfmm/bandlimit.hpp:56-62
+ *   blfmm_bandlimited_radial_table  bandlimited_radial_table(k, sigma, rmax,
+ *                         refinement)                           include/blfmm/bandlimit.hpp:77-79
  *   blfmm_parse_kernel_spec  RadialKernel parse_kernel_spec(const std::string&)
  *                                                               include/blfmm/kernels.hpp:23
  *   blfmm_translation_coefficients  translation_coefficients(k, grid, spectral)
@@ -204,6 +212,26 @@ int blfmm_execute_downsweep(blfmm_plan* plan, double* d_out, blfmm_stats* stats,
 int blfmm_direct(int d, long long n, const double* coords, int kernel_type,
                  double shape, const double* lambda, long long n_targets,
                  const long long* targets, double* out, int device);
+
+/* Band-limited oracles, d = 1 (fmm.cpp:57-70, 77-113): values of
+ * sum_j lambda_j Phi_sigma(x_i - x_j) with Phi_sigma from the cubic-interpolated
+ * radial table over [0, hi[0] - lo[0]] (the domain diameter), or, when
+ * hybrid_leaf_level >= 2, the original kernel for sources in the target's
+ * 3-leaf neighbourhood of build_tree(ps, hybrid_leaf_level) and Phi_sigma
+ * elsewhere (hybrid_leaf_level = -1: the pure band-limited sum). All n
+ * targets into HOST out. d != 1 -> BLFMM_EDOMAIN, as the reference. */
+int blfmm_direct_bandlimited(int d, long long n, const double* coords, const double* lo,
+                             const double* hi, int kernel_type, double shape,
+                             const double* lambda, double sigma, int refinement,
+                             int hybrid_leaf_level, double* out, int device);
+/* Phi_sigma(x) in d = 1 (host, plan-time math; d = 2 -> BLFMM_EDOMAIN). */
+int blfmm_eval_bandlimited(int d, int kernel_type, double shape, double sigma, double x,
+                           int refinement, double* out);
+/* BLFMM_RADIAL_TABLE_SIZE samples of Phi_sigma at step = rmax / 1024 (host,
+ * cached per (kernel, clipped sigma, rmax, refinement) like the reference). */
+#define BLFMM_RADIAL_TABLE_SIZE 1027
+int blfmm_bandlimited_radial_table(int kernel_type, double shape, double sigma, double rmax,
+                                   int refinement, double* vals, double* step);
 
 #ifdef __cplusplus
 }

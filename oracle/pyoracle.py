@@ -304,6 +304,28 @@ def ref_direct(x, w, spec):
     return out, near.value
 
 
+def ref_direct_bl(x, w, spec, sigma, refinement=1024, leaf=-1, lo=None, hi=None):
+    """The reference's band-limited direct oracle (leaf < 0) or its hybrid
+    oracle on build_tree(ps, leaf) (fmm.cpp:57-113); d = 1."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    n, d = x.shape
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    out = np.zeros(n)
+    lo = None if lo is None else np.ascontiguousarray(lo, dtype=np.float64)
+    hi = None if hi is None else np.ascontiguousarray(hi, dtype=np.float64)
+    _chk(ref().ref_direct_bl(d, n, _ptr(x), None if lo is None else _ptr(lo),
+                             None if hi is None else _ptr(hi), _spec_b(spec), _ptr(w),
+                             ct.c_double(sigma), refinement, leaf, _ptr(out)), "ref")
+    return out
+
+
+def ref_eval_bandlimited(spec, sigma, x, refinement=2048):
+    out = ct.c_double()
+    _chk(ref().ref_eval_bandlimited(_spec_b(spec), ct.c_double(sigma), ct.c_double(x),
+                                    refinement, ct.byref(out)), "ref")
+    return out.value
+
+
 def ref_level_c_tables(spec, sigma, m, d, leaf, mode=0, stencil=10):
     """LevelGrids::factors[l].c_vals, l = 2..leaf, as [leaf-1, K]."""
     out = np.zeros((leaf - 1, m ** d))

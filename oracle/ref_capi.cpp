@@ -13,6 +13,9 @@
 //   make_level_grids        core/include/blfmm/mlfmm.hpp:61-63
 //   translation_coefficients core/include/blfmm/bandlimit.hpp:106-108
 //   upsweep / couple        core/include/blfmm/mlfmm.hpp:79-87
+//   direct_matvec (band-limited) / direct_matvec_hybrid
+//                           core/include/blfmm/fmm.hpp:33-43
+//   eval_bandlimited        core/include/blfmm/bandlimit.hpp:56-62
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -214,6 +217,29 @@ int ref_tree_lists(int d, int n, const double* x, const double* lo,
       if (ids)
         for (int v : lists[b]) ids[pos++] = v;
     }
+  });
+}
+
+// Band-limited O(N^2) oracle (use_bandlimited = true) or, leaf >= 0, the
+// hybrid oracle on build_tree(ps, leaf); d = 1.
+int ref_direct_bl(int d, int n, const double* x, const double* lo, const double* hi,
+                  const char* spec, const double* w, double sigma, int refinement, int leaf,
+                  double* out) {
+  return guard([&] {
+    PointSet ps = make_ps(d, n, x, lo, hi);
+    std::vector<double> wv(w, w + n);
+    auto k = parse_kernel_spec(spec);
+    SumResult r = leaf >= 0
+                      ? direct_matvec_hybrid(k, ps, build_tree(ps, leaf), wv, sigma, refinement)
+                      : direct_matvec(k, ps, wv, true, sigma, refinement);
+    std::memcpy(out, r.values.data(), n * sizeof(double));
+  });
+}
+
+int ref_eval_bandlimited(const char* spec, double sigma, double x, int refinement,
+                         double* out) {
+  return guard([&] {
+    *out = eval_bandlimited(parse_kernel_spec(spec), sigma, Pt{x, 0.0}, 1, refinement);
   });
 }
 

@@ -9,7 +9,8 @@ from .api import *  # noqa: F401,F403
 from .api import (AccuracyError, BlfmmError, BoundingBox, BoxTree, CudaError,  # noqa: F401
                   DomainError, GridMode, InvalidArgument, KernelType, LevelGrids,
                   LowRankFactors, Plan, PointSet, QuadratureGrid, RadialKernel, SumRequest,
-                  SumResult, SumStats, build_tree, choose_truncation, couple, direct_matvec,
+                  SumResult, SumStats, bandlimited_radial_table, build_tree, choose_truncation,
+                  couple, direct_matvec, direct_matvec_hybrid, eval_bandlimited,
                   fmm_matvec_single, make_level_grids, make_quadrature, mlfmm_matvec,
                   parse_kernel_spec, translation_coefficients, upsweep)
 

@@ -92,6 +92,13 @@ EXPORTS = {
     "blfmm_direct": (ct.c_int, [ct.c_int, ct.c_longlong, ct.POINTER(ct.c_double), ct.c_int,
                                 ct.c_double, ct.POINTER(ct.c_double), ct.c_longlong,
                                 ct.POINTER(ct.c_longlong), ct.POINTER(ct.c_double), ct.c_int]),
+    "blfmm_direct_bandlimited": (ct.c_int, [ct.c_int, ct.c_longlong, ct.POINTER(ct.c_double), ct.POINTER(ct.c_double), ct.POINTER(ct.c_double), ct.c_int,
+                                            ct.c_double, ct.POINTER(ct.c_double), ct.c_double, ct.c_int, ct.c_int,
+                                            ct.POINTER(ct.c_double), ct.c_int]),
+    "blfmm_eval_bandlimited": (ct.c_int, [ct.c_int, ct.c_int, ct.c_double, ct.c_double,
+                                          ct.c_double, ct.c_int, ct.POINTER(ct.c_double)]),
+    "blfmm_bandlimited_radial_table": (ct.c_int, [ct.c_int, ct.c_double, ct.c_double,
+                                                  ct.c_double, ct.c_int, ct.POINTER(ct.c_double), ct.POINTER(ct.c_double)]),
 }
 
 _lib = None

@@ -485,7 +485,7 @@ def direct_matvec(k: RadialKernel, ps: PointSet, weights, use_bandlimited: bool 
     if w.shape != (n,):
         raise InvalidArgument("weights length != point count")
     if use_bandlimited:
-        raise DomainError("band-limited direct oracle is 1d/host-only; not on the GPU path")
+        return _direct_bandlimited(k, ps, w, sigma, refinement, -1)
     coords = np.ascontiguousarray(ps.pts, dtype=np.float64)
     tg = None if targets is None else np.ascontiguousarray(targets, dtype=np.int64)
     nt = n if tg is None else tg.shape[0]
@@ -495,6 +495,51 @@ def direct_matvec(k: RadialKernel, ps: PointSet, weights, use_bandlimited: bool 
         None if tg is None else tg.ctypes.data_as(ct.POINTER(ct.c_longlong)),
         _ptr(out), -1))
     return SumResult(out, SumStats(n * n if tg is None else n * nt, 0, 0.0))
+
+
+def _direct_bandlimited(k: RadialKernel, ps: PointSet, w, sigma, refinement, leaf_level):
+    n = ps.size()
+    coords = np.ascontiguousarray(ps.pts, dtype=np.float64)
+    lo = np.ascontiguousarray(ps.domain.lo[:ps.d], dtype=np.float64)
+    hi = np.ascontiguousarray(ps.domain.hi[:ps.d], dtype=np.float64)
+    out = np.zeros(n)
+    _capi.check(_capi.lib().blfmm_direct_bandlimited(
+        ps.d, n, _ptr(coords), _ptr(lo), _ptr(hi), int(k.type), k.shape, _ptr(w),
+        float(sigma), int(refinement), int(leaf_level), _ptr(out), -1))
+    return SumResult(out, SumStats(n * n, 0, 0.0))
+
+
+def direct_matvec_hybrid(k: RadialKernel, ps: PointSet, tree: BoxTree, weights,
+                         sigma: float, refinement: int = 1024) -> SumResult:
+    """fmm.cpp:77-113 on the GPU: the original kernel inside the target leaf's
+    neighbour block, Phi_sigma (radial table) outside it; d = 1 only."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    if w.shape != (ps.size(),):
+        raise InvalidArgument("weights length != point count")
+    if ps.d != 1:
+        raise DomainError("hybrid direct oracle is 1d only")
+    return _direct_bandlimited(k, ps, w, sigma, refinement, tree.leaf_level)
+
+
+def eval_bandlimited(k: RadialKernel, sigma: float, x, d: int = 1,
+                     refinement: int = 2048) -> float:
+    """bandlimit.cpp:307-334, d = 1 (host plan-time math of the library)."""
+    out = ct.c_double()
+    x0 = float(x[0]) if np.ndim(x) else float(x)
+    _capi.check(_capi.lib().blfmm_eval_bandlimited(int(d), int(k.type), k.shape, float(sigma),
+                                                   x0, int(refinement), ct.byref(out)))
+    return out.value
+
+
+def bandlimited_radial_table(k: RadialKernel, sigma: float, rmax: float,
+                             refinement: int = 1024):
+    """bandlimit.cpp:241-262: (step, 1027 samples of Phi_sigma on [0, rmax + 2 step])."""
+    vals = np.zeros(1027)
+    step = ct.c_double()
+    _capi.check(_capi.lib().blfmm_bandlimited_radial_table(
+        int(k.type), k.shape, float(sigma), float(rmax), int(refinement), _ptr(vals),
+        ct.byref(step)))
+    return step.value, vals
 
 
 def upsweep(tree: BoxTree, grids: LevelGrids, ps: PointSet, weights):

@@ -26,5 +26,12 @@ void require_fmm_kernel(const KernelSpec& k);
 double fourier_value(const KernelSpec& k, double xi, int d);
 std::vector<double> translation_spectrum(const KernelSpec& k, double sigma,
                                          int m, int d);
+// Phi_sigma in d = 1 (bandlimit.cpp:307-334) and its cubic-interpolation
+// table of kRadialIntervals + 3 samples at step rmax / kRadialIntervals
+// (bandlimit.cpp:229-262).
+constexpr int kRadialIntervals = 1024;
+double eval_bandlimited_1d(const KernelSpec& k, double sigma, double x, int refinement);
+std::vector<double> bandlimited_radial_table(const KernelSpec& k, double sigma, double rmax,
+                                             int refinement, double* step);
 
 }  // namespace blfmm_gpu

@@ -12,10 +12,14 @@
 //   translation_coefficients (spectral) bandlimit.cpp:388-447 with the cell
 //                          averages of bandlimit.cpp:336-384 and their 3-D
 //                          analogue (fold / split / corner / tensor rule).
+//   eval_bandlimited (d=1) bandlimit.cpp:307-334 with the band integrals of
+//                          bandlimit.cpp:61-100 (Gaussian, IMQ, MQ tail form)
+//   bandlimited_radial_table bandlimit.cpp:229-262 (1027 samples, cached)
 #include <algorithm>
 #include <cctype>
 #include <cmath>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -31,11 +35,12 @@ constexpr double kPi = 3.14159265358979323846;
 constexpr double kTwoPi = 2.0 * kPi;
 constexpr double kPoleBall = 1e-8;  // exclusion radius around the spectral pole
 
-// Gauss-Legendre rule with 30 nodes: roots of P_30 by Newton in long double.
-class GaussLegendre30 {
+// Gauss-Legendre rule with N nodes: roots of P_N by Newton in long double.
+template <int N>
+class GaussLegendre {
  public:
-  GaussLegendre30() {
-    constexpr int n = 30;
+  GaussLegendre() {
+    constexpr int n = N;
     for (int i = 0; i < n / 2; ++i) {
       long double z = std::cos(3.14159265358979323846264338L * (i + 0.75L) / (n + 0.5L));
       long double deriv = 0;
@@ -66,15 +71,18 @@ class GaussLegendre30 {
   template <class F>
   double integrate(const F& f, double a, double b) const {
     double mid = 0.5 * (a + b), half = 0.5 * (b - a), acc = 0.0;
-    for (int i = 0; i < 15; ++i)
+    for (int i = 0; i < N / 2; ++i)
       acc += (f(mid + half * node_[i]) + f(mid - half * node_[i])) * weight_[i];
     return half * acc;
   }
+  double node(int i) const { return node_[i]; }
+  double weight(int i) const { return weight_[i]; }
 
  private:
-  double node_[15];
-  double weight_[15];
+  double node_[N / 2];
+  double weight_[N / 2];
 };
+using GaussLegendre30 = GaussLegendre<30>;
 
 const GaussLegendre30& gl() {
   static const GaussLegendre30 rule;
@@ -396,6 +404,110 @@ std::vector<double> translation_spectrum(const KernelSpec& k, double sigma,
   });
   for (long node = 0; node < kk; ++node) c[node] = scale * avg[index[cell_of[node]]];
   return c;
+}
+
+// ---------------------------------------------------------------------------
+// Band-limited kernel Phi_sigma in d = 1 (bandlimit.cpp:307-334): the inverse
+// transform of the spectrum restricted to |xi| < sigma. Host-side plan-time
+// math for the O(N^2) band-limited and hybrid oracles (fmm.cpp:57-113).
+namespace {
+
+// Composite 8-point Gauss-Legendre over `panels` uniform panels of [a, b]
+// (bandlimit.cpp:29-44: the panel count, not the rule order, is the knob).
+template <class F>
+double composite_gl8(const F& f, double a, double b, int panels) {
+  static const GaussLegendre<8> rule;
+  const double h = (b - a) / panels;
+  double sum = 0.0;
+  for (int p = 0; p < panels; ++p) {
+    const double mid = a + (p + 0.5) * h, half = 0.5 * h;
+    double acc = 0.0;
+    for (int q = 0; q < 4; ++q) {
+      const double dx = half * rule.node(q);
+      acc += rule.weight(q) * (f(mid - dx) + f(mid + dx));
+    }
+    sum += acc * half;
+  }
+  return sum;
+}
+
+// Upper integration limit where the spectrum has decayed below ~1e-17 of its
+// scale (bandlimit.cpp:48-58).
+double band_cutoff(const KernelSpec& k, double sigma) {
+  if (k.type == BLFMM_KERNEL_GAUSSIAN) return std::min(sigma, 12.6 * std::sqrt(k.shape) + 1.0);
+  if (k.type == BLFMM_KERNEL_IMQ) return std::min(sigma, 46.0 / k.shape + 1.0);
+  return sigma;
+}
+
+// Adaptive bisection with the 30-point rule on each half, stopped when one
+// more level changes the half-sums by <= tol relative (MQ tail integral).
+template <class F>
+double adaptive_gl30(const F& f, double a, double b, double whole, int depth, double tol) {
+  const double m = 0.5 * (a + b);
+  const double left = gl().integrate(f, a, m), right = gl().integrate(f, m, b);
+  const double both = left + right, diff = std::abs(both - whole);
+  if (depth == 0 || diff <= tol * std::abs(both) || diff < 1e-300) return both;
+  return adaptive_gl30(f, a, m, left, depth - 1, tol) +
+         adaptive_gl30(f, m, b, right, depth - 1, tol);
+}
+
+double plain_kernel(const KernelSpec& k, double r) {  // kernels.cpp:131-161
+  const double c = k.shape;
+  if (k.type == BLFMM_KERNEL_GAUSSIAN) return std::exp(-c * r * r);
+  const double q = std::sqrt(r * r + c * c);
+  return k.type == BLFMM_KERNEL_IMQ ? 1.0 / q : q;
+}
+
+}  // namespace
+
+double eval_bandlimited_1d(const KernelSpec& k, double sigma, double x, int refinement) {
+  if (!(sigma > 0.0)) throw Error(BLFMM_EINVAL, "sigma must be positive");
+  if (refinement < 1024) throw Error(BLFMM_EINVAL, "refinement below reference resolution");
+  require_fmm_kernel(k);
+  const double r = std::abs(x);
+  const double hi = band_cutoff(k, sigma);
+  auto f = [&](double xi) { return fourier_value(k, std::abs(xi), 1) * std::cos(xi * r); };
+  switch (k.type) {
+    case BLFMM_KERNEL_GAUSSIAN:  // bandlimit.cpp:61-68
+      return composite_gl8(f, 0.0, hi, refinement) / kPi;
+    case BLFMM_KERNEL_IMQ: {  // bandlimit.cpp:70-84: K_0's log singularity in a DE head panel
+      const double delta = hi / refinement;
+      const double head = double_exponential(f, 0.0, delta);
+      const double body = refinement > 1 ? composite_gl8(f, delta, hi, refinement - 1) : 0.0;
+      return (head + body) / kPi;
+    }
+    default: {  // MQ, bandlimit.cpp:98-113: Phi - (1/pi) int_sigma^inf Phi^ cos
+      const double top = sigma + 60.0 / k.shape;
+      const double whole = gl().integrate(f, sigma, top);
+      return plain_kernel(k, r) - adaptive_gl30(f, sigma, top, whole, 15, 1e-13) / kPi;
+    }
+  }
+}
+
+std::vector<double> bandlimited_radial_table(const KernelSpec& k, double sigma, double rmax,
+                                             int refinement, double* step) {
+  if (!(rmax > 0.0) || !std::isfinite(rmax)) throw Error(BLFMM_EINVAL, "rmax must be > 0");
+  if (!(sigma > 0.0)) throw Error(BLFMM_EINVAL, "sigma must be positive");
+  if (refinement < 1024) throw Error(BLFMM_EINVAL, "refinement below reference resolution");
+  require_fmm_kernel(k);
+  // process-wide cache keyed like bandlimit.cpp:245-251 (clipped sigma: spectra
+  // decayed to nothing by the band edge give the same table for larger sigma)
+  using Key = std::tuple<int, double, double, double, int>;
+  static std::mutex mu;
+  static std::map<Key, std::vector<double>> cache;
+  const Key key{k.type, k.shape, band_cutoff(k, sigma), rmax, refinement};
+  const double h = rmax / kRadialIntervals;
+  if (step) *step = h;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (auto it = cache.find(key); it != cache.end()) return it->second;
+  }
+  std::vector<double> vals(kRadialIntervals + 3);
+  parallel_for(static_cast<long>(vals.size()), [&](long i) {
+    vals[i] = eval_bandlimited_1d(k, sigma, i * h, refinement);
+  });
+  std::lock_guard<std::mutex> lock(mu);
+  return cache.emplace(key, std::move(vals)).first->second;
 }
 
 }  // namespace blfmm_gpu

@@ -33,8 +33,50 @@ def mlfmm_fixture(name, x, w, spec, sigma, m, leaf, with_direct=False, mode=0, s
     print(name, x.shape, st)
 
 
+def bandlimited_fixture(name, cases):
+    """Band-limited (fmm.cpp:57-70) and hybrid (fmm.cpp:77-113) O(N^2) oracles
+    of the reference, d = 1: one npz holding every case (x_i, w_i, spec_i, ...)."""
+    out = {}
+    for i, (x, w, spec, sigma, refinement, leaf) in enumerate(cases):
+        out[f"x_{i}"] = x
+        out[f"w_{i}"] = w
+        out[f"spec_{i}"] = spec
+        out[f"sigma_{i}"] = sigma
+        out[f"refinement_{i}"] = refinement
+        out[f"leaf_{i}"] = leaf
+        out[f"band_{i}"] = po.ref_direct_bl(x, w, spec, sigma, refinement)
+        if leaf >= 2:
+            out[f"hybrid_{i}"] = po.ref_direct_bl(x, w, spec, sigma, refinement, leaf)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), ncases=len(cases), **out)
+    print(name, len(cases), "cases")
+
+
+def bandlimited_main():
+    cases = [
+        # test_fmm.cpp:68-87 (band-limited table path)
+        (I.generate_quasiuniform(16, 1, 8, 0.5), I.uniform_weights(16, 3), "gaussian:c=1",
+         math.pi, 4096, -1),
+        # test_fmm.cpp:89-107 (two points in leaf 0, two in leaf 3, level 2)
+        (np.array([[0.05], [0.1], [0.9], [0.95]]), np.array([1.0, -2.0, 0.5, 1.5]), "imq:c=1",
+         math.pi, 4096, 2),
+        # test_fmm.cpp:131-152 (256-point IMQ fixture, 16 leaves)
+        (I.generate_quasiuniform(256, 1, 2026, 0.35), I.uniform_weights(256, 99), "imq:c=1",
+         math.pi, 4096, 4),
+        # test_mlfmm.cpp:426-437 (1024-point fixture, 32 leaves)
+        (I.generate_quasiuniform(1024, 1, 2026, 0.35), I.uniform_weights(1024, 99), "imq:c=1",
+         math.pi, 4096, 5),
+        # MQ (tail form) and a narrow Gaussian, uniform points
+        (I.uniform_points(2048, 1, 71), I.uniform_weights(2048, 72), "mq:c=0.05", math.pi, 1024,
+         6),
+        (I.uniform_points(1500, 1, 73), I.uniform_weights(1500, 74), "gaussian:c=16", 20.0, 1024,
+         5),
+    ]
+    bandlimited_fixture("bandlimited_1d_ref", cases)
+
+
 def main():
     assert po.ref_available(), "build oracle/_ref first (make -C oracle)"
+    bandlimited_main()
     W = I.WORKLOADS["P1"]
     x, w = W.make()
     mlfmm_fixture("p1_gaussian_2d_ref", x, w, W.kernel, W.sigma, W.m, W.leaf, with_direct=True)
