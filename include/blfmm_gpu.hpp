@@ -13,6 +13,9 @@
 //   SumResult direct_matvec(const RadialKernel&, const PointSet&,
 //                           const std::vector<double>&, bool, double, int)
 //                                             core/include/blfmm/fmm.hpp:33-36
+//   SumResult direct_matvec_hybrid(const RadialKernel&, const PointSet&,
+//                                  const BoxTree&, const std::vector<double>&,
+//                                  double, int)       core/include/blfmm/fmm.hpp:40-43
 // Errors are rethrown as the reference's exception classes
 // (std::invalid_argument, std::domain_error, blfmm::accuracy_error).
 #pragma once
@@ -189,13 +192,42 @@ inline SumResult fmm_matvec_single(const SumRequest& req, const BoxTree& tree) {
   return run(p, req.weights, true);
 }
 
-// fmm.cpp:30-75 plain-kernel O(N^2) sum (use_bandlimited = false).
+// Band-limited (leaf < 0, fmm.cpp:57-70) or hybrid (fmm.cpp:77-113) O(N^2)
+// oracle on the GPU; d = 1 (std::domain_error otherwise, as the reference).
+inline SumResult detail_direct_bandlimited(const RadialKernel& k, const PointSet& ps,
+                                           const std::vector<double>& weights, double sigma,
+                                           int refinement, int leaf) {
+  const int n = ps.size();
+  if (static_cast<int>(weights.size()) != n)
+    throw std::invalid_argument("weights length != point count");
+  std::vector<double> coords(n);
+  for (int i = 0; i < n; ++i) coords[i] = ps.pts[i][0];
+  const double lo[2] = {ps.domain.lo[0], ps.domain.lo[1]};
+  const double hi[2] = {ps.domain.hi[0], ps.domain.hi[1]};
+  SumResult res;
+  res.values.assign(n, 0.0);
+  check(blfmm_direct_bandlimited(ps.d, n, coords.data(), lo, hi, static_cast<int>(k.type),
+                                 k.shape, weights.data(), sigma, refinement, leaf,
+                                 res.values.data(), -1));
+  res.stats.near_pairs = static_cast<long long>(n) * n;
+  return res;
+}
+
+// fmm.cpp:77-113: original kernel in the target leaf's neighbour block,
+// Phi_sigma elsewhere (include/blfmm/fmm.hpp:40-43).
+inline SumResult direct_matvec_hybrid(const RadialKernel& k, const PointSet& ps,
+                                      const BoxTree& tree, const std::vector<double>& weights,
+                                      double sigma, int refinement = 1024) {
+  if (ps.d != 1) throw std::domain_error("hybrid direct oracle is 1d only");
+  return detail_direct_bandlimited(k, ps, weights, sigma, refinement, tree.leaf_level);
+}
+
+// fmm.cpp:30-75 O(N^2) sum: plain kernel, or the band-limited table oracle.
 inline SumResult direct_matvec(const RadialKernel& k, const PointSet& ps,
                                const std::vector<double>& weights, bool use_bandlimited,
                                double sigma, int refinement = 1024) {
-  if (use_bandlimited)  // the 1-D band-limited table oracle stays the reference's CPU code
-    return ::blfmm::direct_matvec(k, ps, weights, true, sigma, refinement);
   const int n = ps.size();
+  if (use_bandlimited) return detail_direct_bandlimited(k, ps, weights, sigma, refinement, -1);
   if (static_cast<int>(weights.size()) != n)
     throw std::invalid_argument("weights length != point count");
   std::vector<double> coords(static_cast<std::size_t>(n) * ps.d);

@@ -47,7 +47,8 @@ def bandlimited_fixture(name, cases):
         out[f"band_{i}"] = po.ref_direct_bl(x, w, spec, sigma, refinement)
         if leaf >= 2:
             out[f"hybrid_{i}"] = po.ref_direct_bl(x, w, spec, sigma, refinement, leaf)
-    np.savez_compressed(os.path.join(HERE, name + ".npz"), ncases=len(cases), **out)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), kind="bandlimited", ncases=len(cases),
+                        **out)
     print(name, len(cases), "cases")
 
 
