@@ -558,6 +558,21 @@ def test_split_symmetric_items_bit_identical(blfmm, monkeypatch):
     assert np.array_equal(alt.values, base.values)
 
 
+def test_p2m_chunk_pipelines_bit_identical(blfmm, monkeypatch):
+    """The fused P2M + leaf M2M kernel's point-chunk staging variants
+    (single-buffered 16-point chunks, double-buffered 8- or 16-point chunks)
+    run the same 4-point DMMA k steps in the same order: bit-identical u and
+    leaf multipoles."""
+    W = I.WORKLOADS["P3"]
+    x, w = W.make(40000)
+    out = []
+    for v in ("0", "1", "2"):
+        monkeypatch.setenv("BLFMM_P2M_VARIANT", v)
+        res, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, 4)
+        out.append(res.values)
+    assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
+
+
 def blfmm_leaf_ids(x, leaf):
     """Row-major leaf ids with the reference's clamp binning (geometry.cpp:254-262)."""
     n = 1 << leaf
