@@ -185,6 +185,36 @@ def test_telescope_3d(oracle):
     assert st["near_pairs"] == st2["near_pairs"]
 
 
+@pytest.mark.parametrize("d,spec,m,leaf,n", [(3, "imq:c=0.1", 8, 3, 600),
+                                              (3, "gaussian:c=4", 6, 2, 500),
+                                              (3, "mq:c=0.2", 6, 3, 400),
+                                              (2, "imq:c=0.1", 12, 4, 700)])
+def test_multilevel_equals_lowrank_split_sum(oracle, d, spec, m, leaf, n):
+    """The restated multilevel sweep equals the method's defining near/far sum
+    (tests/lowrank_split.py), computed without any tree translation."""
+    from tests.lowrank_split import lowrank_split_sum
+    x = I.blob_points(n, 500 + d, 600 + d) if d == 3 else I.uniform_points(n, d, 71)
+    w = I.uniform_weights(n, 72)
+    want = lowrank_split_sum(x, w, spec, math.pi, m, leaf, oracle.c_table(spec, math.pi, m, d))
+    got, _, _ = oracle.mlfmm(x, w, spec, math.pi, m, leaf)
+    assert rel_l2(got, want) <= 1e-12
+
+
+def test_lowrank_split_sum_is_the_reference_2d(oracle):
+    """d = 2: the same identity holds for the reference itself, so the split sum
+    used to pin d = 3 is the reference's own definition of the matvec."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    from tests.lowrank_split import lowrank_split_sum
+    x = I.uniform_points(700, 2, 73)
+    w = I.uniform_weights(700, 74)
+    for spec, m, leaf in [("imq:c=0.1", 12, 4), ("gaussian:c=16", 16, 3), ("mq:c=0.05", 10, 3)]:
+        want = lowrank_split_sum(x, w, spec, math.pi, m, leaf,
+                                 oracle.ref_c_table(spec, math.pi, m, 2))
+        got, _ = oracle.ref_mlfmm(x, w, spec, math.pi, m, leaf)
+        assert rel_l2(got, want) <= 1e-12, spec
+
+
 def test_c_table_3d_gaussian_closed_form(oracle):
     sigma, m, c = math.pi, 6, 64.0
     tab = oracle.c_table(f"gaussian:c={c}", sigma, m, 3)

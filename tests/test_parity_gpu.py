@@ -541,6 +541,23 @@ def test_near_field_schedules_agree(blfmm, oracle, env, monkeypatch):
     assert alt.stats.near_pairs == base.stats.near_pairs
 
 
+@pytest.mark.parametrize("spec,m,leaf,n", [("imq:c=0.1", 16, 3, 800), ("imq:c=0.1", 16, 4, 3000),
+                                          ("gaussian:c=64", 16, 3, 1000), ("mq:c=0.2", 8, 3, 600)])
+def test_gpu_equals_lowrank_split_sum_3d(blfmm, spec, m, leaf, n):
+    """The 3-D GPU path (M = 16: half spectrum, fused P2M + leaf M2M, telescoped
+    couple, symmetric persistent near field) equals the method's defining
+    near/far sum (tests/lowrank_split.py) with the plan's own C table: no tree
+    translation is involved on the checking side."""
+    from tests.lowrank_split import lowrank_split_sum
+    x = I.blob_points(n, 800 + leaf, 900 + leaf)
+    w = I.uniform_weights(n, 77)
+    k = blfmm.parse_kernel_spec(spec)
+    ctab = blfmm.translation_coefficients(k, blfmm.make_quadrature(math.pi, m, 3)).c_vals
+    want = lowrank_split_sum(x, w, spec, math.pi, m, leaf, ctab)
+    res, _ = gpu_mlfmm(blfmm, x, w, spec, math.pi, m, leaf)
+    assert rel_l2(res.values, want) <= 1e-12
+
+
 def test_split_symmetric_items_bit_identical(blfmm, monkeypatch):
     """Symmetric pair items with more than 96 targets run as 96-target chunk
     items (one warp each) whose source-side partials are summed in chunk
