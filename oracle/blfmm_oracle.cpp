@@ -11,8 +11,10 @@
 // Pinning: the d <= 2 instantiation is checked against the reference itself
 // (oracle/_ref/libblfmm_ref.so, compiled from the reference's own sources) and
 // against the reference tests' golden values (tests/test_oracle.py). The d = 3
-// instantiation has no reference counterpart ("parity unpinned" beyond the
-// restatement for 3-D singular C tables). Empty boxes are not
+// instantiation has no reference counterpart; it is pinned by the method's
+// defining near/far low-rank sum, which the reference satisfies in d = 2
+// (tests/lowrank_split.py). Only its 3-D singular C tables rest on the
+// restatement alone, checked by independent quadrature. Empty boxes are not
 // allocated: every skipped term is an exact zero in the reference (x + 0*y ==
 // x for finite y), so this "sparse" storage is result-identical to the
 // reference's dense allocation (mlfmm.cpp:206-216, 273-282).
