@@ -71,6 +71,11 @@ def bandlimited_main():
          6),
         (I.uniform_points(1500, 1, 73), I.uniform_weights(1500, 74), "gaussian:c=16", 20.0, 1024,
          5),
+        # edge cases: a single point (r = 0 only), and points outside the domain
+        # [0, 1] (clamped leaves, distances past rmax: the table's end interval)
+        (np.array([[0.5]]), np.array([2.0]), "imq:c=1", math.pi, 1024, 2),
+        (I.uniform_points(300, 1, 75) * 1.4 - 0.2, I.uniform_weights(300, 76), "imq:c=0.5",
+         math.pi, 1024, 3),
     ]
     bandlimited_fixture("bandlimited_1d_ref", cases)
 
