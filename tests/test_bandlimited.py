@@ -108,11 +108,16 @@ def test_gpu_bandlimited_and_hybrid_match_reference(blfmm):
         r = blfmm.direct_matvec(k, ps, w, use_bandlimited=True, sigma=sigma,
                                 refinement=refinement)
         assert r.stats.near_pairs == len(w) ** 2
-        assert rel_l2(r.values, band) <= 1e-12, (spec, len(w))
+        # Points outside the domain put distances past rmax, where both
+        # implementations extrapolate the end interval's cubic with t up to
+        # ~400: rounding-level table differences grow by ~t^3/6.
+        outside = x.min() < 0.0 or x.max() > 1.0
+        tol = 1e-8 if outside else 1e-12
+        assert rel_l2(r.values, band) <= tol, (spec, len(w))
         if hybrid is not None:
             h = blfmm.direct_matvec_hybrid(k, ps, blfmm.build_tree(ps, leaf), w, sigma,
                                            refinement)
-            assert rel_l2(h.values, hybrid) <= 1e-12, (spec, len(w), leaf)
+            assert rel_l2(h.values, hybrid) <= tol, (spec, len(w), leaf)
 
 
 @pytest.mark.gpu

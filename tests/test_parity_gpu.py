@@ -575,6 +575,22 @@ def test_split_symmetric_items_bit_identical(blfmm, monkeypatch):
     assert np.array_equal(alt.values, base.values)
 
 
+def test_near_register_cap_and_ctas_bit_identical(blfmm, monkeypatch):
+    """The deep-tree near-field configuration (2 persistent CTAs per SM of the
+    80-register k_near_all, the default for 3-D leaf level >= 6) and the
+    shallow one (3 CTAs, uncapped) write the same per-neighbour planes in the
+    same order: bit-identical u."""
+    W = I.WORKLOADS["P3"]
+    x, w = W.make(60000)
+    out = []
+    for minb, persist in (("1", "3"), ("6", "2"), ("6", "3")):
+        monkeypatch.setenv("BLFMM_NEAR_MINB", minb)
+        monkeypatch.setenv("BLFMM_NEAR_PERSIST", persist)
+        res, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, 4)
+        out.append(res.values)
+    assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
+
+
 def test_p2m_chunk_pipelines_bit_identical(blfmm, monkeypatch):
     """The fused P2M + leaf M2M kernel's point-chunk staging variants
     (single-buffered 16-point chunks, double-buffered 8- or 16-point chunks)
