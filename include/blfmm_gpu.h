@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define BLFMM_GPU_ABI_VERSION 2
+#define BLFMM_GPU_ABI_VERSION 3
 
 /* Status codes (reference exception class in parentheses). */
 enum blfmm_status {
@@ -118,7 +118,27 @@ typedef struct blfmm_plan_info {
                                the Hermitian half spectrum (3-D, M = 16: 2528) */
   int telescoped;           /* 1: execute evaluates G_L from the root multipole
                                (leaf-level couple only) */
+  long long near_sym_items; /* symmetric near-field items (leaf pairs evaluated
+                               once for both sides; nrhs = 1) */
+  long long near_items;     /* one-sided near-field items (up to 96 targets) */
+  char kernels[256];        /* the kernel each stage of blfmm_execute launches,
+                               "p2m=... m2m=... couple=... l2p=... near=..." */
 } blfmm_plan_info;
+
+/* Optional plan tuning (blfmm_plan_create_tuned). blfmm_tuning_defaults
+ * fills the values blfmm_plan_create uses; every field selects between
+ * kernels or schedules of the same matvec (results agree to rounding). */
+typedef struct blfmm_tuning {
+  int telescope;        /* 1: 3-D shared grids evaluate the leaf locals from the
+                           root multipole (one leaf-level couple launch);
+                           0: level-by-level couple + L2L sweep (mlfmm.cpp:268-340) */
+  int graphs;           /* 1: replay the launch sequence as a CUDA graph */
+  int near_sym_min;     /* symmetric near-field items for neighbouring leaves
+                           that both hold >= this many points (0: off) */
+  int near_ctas_per_sm; /* persistent near-field CTAs per SM (0: plan heuristic) */
+  int near_reg_cap;     /* near-field register cap: 80, or 255 uncapped
+                           (0: plan heuristic) */
+} blfmm_tuning;
 
 /* Per-stage device times of the last execute (CUDA events on the launch
  * stream), enabled by blfmm_set_profiling. Order: tree/gather, p2m, m2m,
@@ -142,6 +162,9 @@ int blfmm_translation_coefficients(int d, int kernel_type, double shape,
                                    double sigma, int m_per_dim, double* c_out);
 
 int blfmm_plan_create(const blfmm_plan_desc* desc, blfmm_plan** out);
+void blfmm_tuning_defaults(blfmm_tuning* t);
+int blfmm_plan_create_tuned(const blfmm_plan_desc* desc, const blfmm_tuning* tuning,
+                            blfmm_plan** out);
 int blfmm_plan_destroy(blfmm_plan* plan);
 int blfmm_plan_get_info(const blfmm_plan* plan, blfmm_plan_info* info);
 

@@ -49,6 +49,13 @@ struct Kernel {
 
 thread_local std::string g_err;
 int g_mode = 0, g_stencil = 10;
+// Optional target subset (parity checks at sizes where the full far field is
+// too slow on the host): the dense leaf ids whose points are evaluated. The
+// upsweep still runs over every box (all sources); couple, L2L, L2P and the
+// near field run only on the selected leaves and their ancestors, with the
+// same per-box arithmetic as the full sweep, so the selected targets' values
+// are those of the full matvec. Empty = every leaf.
+std::vector<long> g_target_leaves;
 
 // ---------------------------------------------------------------- kernels
 // eval_kernel, kernels.cpp:131-161
@@ -711,6 +718,27 @@ std::vector<long> occupied(const Tree& t, int l, int stride) {
   return v;
 }
 
+// Boxes of level l that are ancestors of (or are) a selected target leaf.
+std::vector<char> target_chain(const Tree& t, int l) {
+  std::vector<char> on(t.count(l), g_target_leaves.empty() ? 1 : 0);
+  for (long a : g_target_leaves) {
+    long i[3];
+    t.idx(t.L, a, i);
+    for (int k = 0; k < t.d; ++k) i[k] >>= (t.L - l);
+    on[t.id(l, i)] = 1;
+  }
+  return on;
+}
+std::vector<long> occupied_targets(const Tree& t, int l, int stride) {
+  auto v = occupied(t, l, stride);
+  if (g_target_leaves.empty()) return v;
+  auto on = target_chain(t, l);
+  std::vector<long> out;
+  for (long b : v)
+    if (on[b]) out.push_back(b);
+  return out;
+}
+
 // upsweep, mlfmm.cpp:201-266 (shared grids)
 std::vector<Level> upsweep(const Problem& p, const Tree& t, const Grids& G,
                            const double* w, Sampler* s) {
@@ -790,7 +818,7 @@ std::vector<Level> couple(const Problem& p, const Tree& t, const Grids& G,
   double tc = timed([&] {
     for (int l = 2; l <= L; ++l) {
       loc[l].resize(t.count(l));
-      auto targets = occupied(t, l, stride);
+      auto targets = occupied_targets(t, l, stride);
 #pragma omp parallel for schedule(dynamic)
       for (long q = 0; q < (long)targets.size(); ++q) {
         long a = targets[q];
@@ -827,7 +855,7 @@ void downsweep(const Problem& p, const Tree& t, const Grids& G,
   double tcopy = timed([&] { acc = locals; });  // mlfmm.cpp:305
   double tl = timed([&] {
     for (int l = 2; l < L; ++l) {
-      auto parents = occupied(t, l, stride);
+      auto parents = occupied_targets(t, l, stride);
 #pragma omp parallel for schedule(dynamic)
       for (long q = 0; q < (long)parents.size(); ++q) {
         long pb = parents[q];
@@ -858,7 +886,7 @@ void downsweep(const Problem& p, const Tree& t, const Grids& G,
     }
   });
   double imag = 0.0;
-  auto leaves = occupied(t, L, stride);
+  auto leaves = occupied_targets(t, L, stride);
   double tp = timed([&] {
 #pragma omp parallel for schedule(dynamic) reduction(max : imag)
     for (long q = 0; q < (long)leaves.size(); ++q) {
@@ -920,7 +948,7 @@ void mlfmm(const Problem& p, const Grids& G, const double* w, double* out, Stats
   loc.clear();
   int L = t.L, stride = s ? s->stride : 1;
   long long near = 0;
-  auto leaves = occupied(t, L, stride);
+  auto leaves = occupied_targets(t, L, stride);
   double tn = timed([&] {
 #pragma omp parallel for schedule(dynamic) reduction(+ : near)
     for (long q = 0; q < (long)leaves.size(); ++q) {
@@ -1088,6 +1116,11 @@ void orc_set_grid_mode(int mode, int stencil_k) {
 
 // bench.py's CPU legs: use every host thread even when a launcher (torchrun)
 // exported OMP_NUM_THREADS=1 before this library was loaded.
+// Target-leaf subset for the following orc_mlfmm calls (n = 0: all leaves).
+void orc_set_target_leaves(long n, const long* leaf_ids) {
+  g_target_leaves.assign(leaf_ids, leaf_ids + (n > 0 ? n : 0));
+}
+
 void orc_set_num_threads(int n) {
   if (n > 0) omp_set_num_threads(n);
 }

@@ -233,6 +233,37 @@ class grid_mode:
             ref().ref_set_grid_mode(0, 10)
 
 
+class target_leaves:
+    """Context: restrict the oracle's couple / L2L / L2P / near field to the
+    given dense leaf ids (row-major, level ``leaf``) and their ancestors; the
+    upsweep still covers every source. Values are those of the full matvec
+    at the points of the selected leaves (other entries are not evaluated)."""
+
+    def __init__(self, ids):
+        self.ids = np.ascontiguousarray(np.asarray(ids, dtype=np.int64))
+
+    def __enter__(self):
+        lib().orc_set_target_leaves(ct.c_long(self.ids.size), _ptr(self.ids, _lp))
+        return self
+
+    def __exit__(self, *a):
+        lib().orc_set_target_leaves(ct.c_long(0), None)
+
+
+def leaf_ids(x, leaf, lo=None, hi=None):
+    """Dense row-major leaf id of every point (leaf_of, geometry.cpp:254-262)."""
+    x = np.asarray(x, dtype=np.float64)
+    n, d = x.shape
+    lo3, hi3 = _box(d, lo, hi)
+    nper = 1 << leaf
+    ids = np.zeros(n, dtype=np.int64)
+    for k in range(d):
+        side = (hi3[k] - lo3[k]) / nper
+        v = ((x[:, k] - lo3[k]) / side).astype(np.int64)
+        ids = ids * nper + np.clip(v, 0, nper - 1)
+    return ids
+
+
 def set_threads(n: int) -> int:
     """omp_set_num_threads for the oracle (returns the resulting max threads)."""
     lib().orc_set_num_threads(int(n))

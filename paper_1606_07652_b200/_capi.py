@@ -52,7 +52,15 @@ class PlanInfo(ct.Structure):
         ("owned_begin", ct.c_longlong), ("owned_end", ct.c_longlong),
         ("plan_seconds", ct.c_double), ("device_bytes", ct.c_longlong),
         ("stored_nodes", ct.c_longlong), ("telescoped", ct.c_int),
+        ("near_sym_items", ct.c_longlong), ("near_items", ct.c_longlong),
+        ("kernels", ct.c_char * 256),
     ]
+
+
+class Tuning(ct.Structure):
+    """blfmm_tuning (include/blfmm_gpu.h): kernel / schedule selection."""
+    _fields_ = [("telescope", ct.c_int), ("graphs", ct.c_int), ("near_sym_min", ct.c_int),
+                ("near_ctas_per_sm", ct.c_int), ("near_reg_cap", ct.c_int)]
 
 
 class StageTimes(ct.Structure):
@@ -69,6 +77,9 @@ EXPORTS = {
                                                   ct.c_int, ct.POINTER(ct.c_double)]),
     "blfmm_plan_create": (ct.c_int, [ct.POINTER(PlanDesc), ct.POINTER(ct.c_void_p)]),
     "blfmm_plan_destroy": (ct.c_int, [ct.c_void_p]),
+    "blfmm_tuning_defaults": (None, [ct.POINTER(Tuning)]),
+    "blfmm_plan_create_tuned": (ct.c_int, [ct.POINTER(PlanDesc), ct.POINTER(Tuning),
+                                           ct.POINTER(ct.c_void_p)]),
     "blfmm_plan_get_info": (ct.c_int, [ct.c_void_p, ct.POINTER(PlanInfo)]),
     "blfmm_execute": (ct.c_int, [ct.c_void_p, ct.POINTER(ct.c_double), ct.POINTER(ct.c_double),
                                  ct.POINTER(Stats), ct.c_void_p]),

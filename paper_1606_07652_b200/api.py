@@ -312,7 +312,7 @@ class Plan:
     def __init__(self, ps: PointSet, leaf_level: int, kernel: RadialKernel, sigma: float,
                  m_per_dim: int, c_table: np.ndarray | None = None, nrhs: int = 1,
                  device: int = -1, rank: int = 0, world: int = 1, grid_mode: int = 0,
-                 stencil_k: int = 10):
+                 stencil_k: int = 10, tuning: dict | None = None):
         self._h = ct.c_void_p()
         self._keep = []
         d = ps.d
@@ -340,7 +340,14 @@ class Plan:
             desc.c_table = _ptr(ctab)
         desc.rank = rank
         desc.world = world
-        _capi.check(_capi.lib().blfmm_plan_create(ct.byref(desc), ct.byref(self._h)))
+        tune = _capi.Tuning()
+        _capi.lib().blfmm_tuning_defaults(ct.byref(tune))
+        for k, v in (tuning or {}).items():
+            if not hasattr(tune, k):
+                raise InvalidArgument(f"unknown tuning field {k!r}")
+            setattr(tune, k, int(v))
+        _capi.check(_capi.lib().blfmm_plan_create_tuned(ct.byref(desc), ct.byref(tune),
+                                                        ct.byref(self._h)))
         self.n, self.d, self.nrhs = ps.size(), d, nrhs
         self.K = m_per_dim ** d
         self.leaf_level = leaf_level
@@ -354,6 +361,14 @@ class Plan:
         inf = _capi.PlanInfo()
         _capi.check(_capi.lib().blfmm_plan_get_info(self._h, ct.byref(inf)))
         return inf
+
+    def kernels(self) -> dict:
+        """Stage -> kernel that blfmm_execute launches (blfmm_plan_info.kernels)."""
+        out = {}
+        for tok in self.info().kernels.decode().split():
+            k, _, v = tok.partition("=")
+            out[k] = v
+        return out
 
     def _weights(self, weights):
         w = np.ascontiguousarray(weights, dtype=np.float64)

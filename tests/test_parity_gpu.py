@@ -26,7 +26,7 @@ def rel_l2(a, b):
 
 
 def gpu_mlfmm(B, x, w, spec, sigma, m, leaf, lo=None, hi=None, c_table=None, grid_mode=0,
-              stencil_k=10):
+              stencil_k=10, tuning=None):
     d = x.shape[1]
     dom = B.BoundingBox(tuple(lo) if lo is not None else (0.0,) * 3,
                         tuple(hi) if hi is not None else (1.0,) * 3)
@@ -34,7 +34,7 @@ def gpu_mlfmm(B, x, w, spec, sigma, m, leaf, lo=None, hi=None, c_table=None, gri
     w = np.asarray(w)
     plan = B.Plan(ps, leaf, B.parse_kernel_spec(spec), sigma, m, c_table=c_table,
                   nrhs=1 if w.ndim == 1 else w.shape[0], grid_mode=grid_mode,
-                  stencil_k=stencil_k)
+                  stencil_k=stencil_k, tuning=tuning)
     return plan.execute(w), plan
 
 
@@ -283,9 +283,8 @@ def test_full_size_p3_properties(blfmm):
 @pytest.mark.parametrize("name,n,leaf", [("P3", 60000, 4), ("P4", 50000, 5), ("P1", 4096, 3)])
 def test_sharded_plans_assemble_to_full(blfmm, name, n, leaf):
     """Morton-range sharding: the owned outputs of world plans (one per rank,
-    here all on one GPU, no collective) sum to the single-plan matvec (up to
-    the re-association of split near-field items), and the owned near-pair
-    counts add up."""
+    here all on one GPU, no collective) sum to the single-plan matvec, and the
+    owned near-pair counts add up."""
     W = I.WORKLOADS[name]
     x, w = W.make(n)
     k = blfmm.parse_kernel_spec(W.kernel)
@@ -302,9 +301,9 @@ def test_sharded_plans_assemble_to_full(blfmm, name, n, leaf):
             pairs += r.stats.near_pairs
             inf = pl.info()
             owned.append(inf.owned_end - inf.owned_begin)
-        # bit-identical unless near-field items were split on the sharded plans
-        # (3 partial sums re-associated): rounding level
-        assert np.abs(acc - full.values).max() <= 1e-14 * np.abs(full.values).max(), world
+        # every target's near and far sums are formed by the same items in the
+        # same order on its owning rank: bit-identical
+        assert np.array_equal(acc, full.values), world
         assert pairs == full.stats.near_pairs
         assert sum(owned) == n
 
@@ -468,7 +467,7 @@ def test_scaled_mode_validation(blfmm):
         blfmm.Plan(ps, 3, k, math.pi, 8, grid_mode=1, rank=0, world=2)
 
 
-def test_graph_replay_matches_direct_launch(blfmm, monkeypatch):
+def test_graph_replay_matches_direct_launch(blfmm):
     """execute_device captures the launch sequence into a CUDA graph on the
     second use of a (lambda, out) pointer pair and replays it afterwards; the
     replayed matvec equals a plan that launches directly, bit for bit."""
@@ -479,9 +478,8 @@ def test_graph_replay_matches_direct_launch(blfmm, monkeypatch):
     ps = blfmm.PointSet(W.d, x)
     lam = torch.from_numpy(np.ascontiguousarray(w.reshape(1, -1))).cuda()
     outs = []
-    for graphs in ("1", "0"):
-        monkeypatch.setenv("BLFMM_GRAPHS", graphs)
-        plan = blfmm.Plan(ps, 4, k, W.sigma, W.m)
+    for graphs in (1, 0):
+        plan = blfmm.Plan(ps, 4, k, W.sigma, W.m, tuning={"graphs": graphs})
         out = torch.empty_like(lam)
         for _ in range(4):  # direct, capture + replay, replay, replay
             out.zero_()
@@ -493,7 +491,7 @@ def test_graph_replay_matches_direct_launch(blfmm, monkeypatch):
 
 
 @pytest.mark.parametrize("name,n,leaf", [("P3", 40000, 4), ("P2p", 20000, 4), ("P5", 8192, 3)])
-def test_telescoped_equals_level_sweep(blfmm, oracle, name, n, leaf, monkeypatch):
+def test_telescoped_equals_level_sweep(blfmm, oracle, name, n, leaf):
     """Shared grids make G_l a pure shift of G_1 = C V_0:
     execute evaluates the leaf locals from the root multipole and skips the
     level 1..L-1 couple launches. It equals the level-by-level G recursion to
@@ -503,12 +501,12 @@ def test_telescoped_equals_level_sweep(blfmm, oracle, name, n, leaf, monkeypatch
     if w.ndim == 2:
         w = w[:16]
     res = {}
-    for tv in ("0", "1"):
-        monkeypatch.setenv("BLFMM_TELESCOPE", tv)
-        r, plan = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
-        assert plan.info().telescoped == int(tv)
+    for tv in (0, 1):
+        r, plan = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf, tuning={"telescope": tv})
+        assert plan.info().telescoped == tv
+        assert plan.kernels()["couple"] == ("k_root+k_couple3<ROOT>" if tv else "k_couple3")
         res[tv] = r
-    a, b = res["1"], res["0"]
+    a, b = res[1], res[0]
     assert rel_l2(a.values, b.values) <= 1e-13, rel_l2(a.values, b.values)
     assert a.stats.near_pairs == b.stats.near_pairs and a.stats.far_work == b.stats.far_work
     assert abs(a.stats.max_imag_residual - b.stats.max_imag_residual) <= \
@@ -519,24 +517,24 @@ def test_telescoped_equals_level_sweep(blfmm, oracle, name, n, leaf, monkeypatch
     assert rel_l2(a.values, ov) <= TOL
 
 
-@pytest.mark.parametrize("env", [{"BLFMM_NEAR_SYM": "0"}, {"BLFMM_NEAR_PERSIST": "0"},
-                                 {"BLFMM_NEAR_SYM": "8", "BLFMM_NEAR_PERSIST": "2"},
-                                 {"BLFMM_NEAR_STAGE": "0"}])
-def test_near_field_schedules_agree(blfmm, oracle, env, monkeypatch):
-    """The symmetric pair kernel (phi once per unordered pair of large
-    neighbouring leaves, per-neighbour planes), the persistent queue and the
-    one-sided kernels are the same near field: every configuration equals the
-    default one to rounding, and repeated executes are bit-identical (fixed
-    summation order, no atomics on values)."""
-    W = I.WORKLOADS["P3"]
+@pytest.mark.parametrize("tuning", [{"near_sym_min": 0}, {"near_sym_min": 8},
+                                    {"near_ctas_per_sm": 1},
+                                    {"near_ctas_per_sm": 3, "near_reg_cap": 80}])
+@pytest.mark.parametrize("name,leaf", [("P3", 4), ("P4", 6)])
+def test_near_field_schedules_agree(blfmm, oracle, tuning, name, leaf):
+    """The symmetric pair items (phi once per unordered pair of large
+    neighbouring leaves, per-neighbour planes) and the one-sided items are the
+    same near field whatever the threshold and the persistent grid: every
+    configuration equals the default one to rounding, and repeated executes
+    are bit-identical (fixed summation order, no atomics on values)."""
+    W = I.WORKLOADS[name]
     x, w = W.make(60000)
-    leaf = 4  # 4096 leaves, ~15 points each: sym, one-sided and G-split items all occur
     base, plan = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
     again = plan.execute(w)
     assert np.array_equal(base.values, again.values)
-    for k_, v in env.items():
-        monkeypatch.setenv(k_, v)
-    alt, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
+    alt, aplan = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf, tuning=tuning)
+    if tuning.get("near_sym_min") == 0:
+        assert aplan.info().near_sym_items == 0
     assert rel_l2(alt.values, base.values) <= 1e-13, rel_l2(alt.values, base.values)
     assert alt.stats.near_pairs == base.stats.near_pairs
 
@@ -558,24 +556,7 @@ def test_gpu_equals_lowrank_split_sum_3d(blfmm, spec, m, leaf, n):
     assert rel_l2(res.values, want) <= 1e-12
 
 
-def test_split_symmetric_items_bit_identical(blfmm, monkeypatch):
-    """Symmetric pair items with more than 96 targets run as 96-target chunk
-    items (one warp each) whose source-side partials are summed in chunk
-    order by k_sym_fix: the same operations in the same order as one warp's
-    sequential passes, so the result is bit-identical to the unsplit queue."""
-    W = I.WORKLOADS["P3"]
-    x, w = W.make(60000)
-    leaf = 4
-    counts = np.bincount(blfmm_leaf_ids(x, leaf), minlength=8 ** leaf)
-    assert counts.max() > 96  # the split path is exercised
-    monkeypatch.setenv("BLFMM_SYM_SPLIT", "1")
-    base, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
-    monkeypatch.setenv("BLFMM_SYM_SPLIT", "0")
-    alt, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
-    assert np.array_equal(alt.values, base.values)
-
-
-def test_near_register_cap_and_ctas_bit_identical(blfmm, monkeypatch):
+def test_near_register_cap_and_ctas_bit_identical(blfmm):
     """The deep-tree near-field configuration (2 persistent CTAs per SM of the
     80-register k_near_all, the default for 3-D leaf level >= 6) and the
     shallow one (3 CTAs, uncapped) write the same per-neighbour planes in the
@@ -583,25 +564,9 @@ def test_near_register_cap_and_ctas_bit_identical(blfmm, monkeypatch):
     W = I.WORKLOADS["P3"]
     x, w = W.make(60000)
     out = []
-    for minb, persist in (("1", "3"), ("6", "2"), ("6", "3")):
-        monkeypatch.setenv("BLFMM_NEAR_MINB", minb)
-        monkeypatch.setenv("BLFMM_NEAR_PERSIST", persist)
-        res, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, 4)
-        out.append(res.values)
-    assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
-
-
-def test_p2m_chunk_pipelines_bit_identical(blfmm, monkeypatch):
-    """The fused P2M + leaf M2M kernel's point-chunk staging variants
-    (single-buffered 16-point chunks, double-buffered 8- or 16-point chunks)
-    run the same 4-point DMMA k steps in the same order: bit-identical u and
-    leaf multipoles."""
-    W = I.WORKLOADS["P3"]
-    x, w = W.make(40000)
-    out = []
-    for v in ("0", "1", "2"):
-        monkeypatch.setenv("BLFMM_P2M_VARIANT", v)
-        res, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, 4)
+    for cap, ctas in ((255, 3), (80, 2), (80, 3)):
+        res, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, 4,
+                           tuning={"near_reg_cap": cap, "near_ctas_per_sm": ctas})
         out.append(res.values)
     assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
 

@@ -1,5 +1,7 @@
 """Device-timed matvec loop (no per-stage fences): prints ms per matvec for a
-BASELINE workload. Used for A/B runs of the env knobs (BLFMM_*)."""
+BASELINE workload, then one serialised per-stage profile. --tuning takes a
+JSON dict of blfmm_tuning fields for A/B runs."""
+import json
 import argparse
 import ctypes as ct
 import os
@@ -21,13 +23,15 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--tag", default="")
     ap.add_argument("--scaled", type=int, default=0, help="GridMode::scaled with this stencil")
+    ap.add_argument("--tuning", default="{}")
     args = ap.parse_args()
     W = I.WORKLOADS[args.workload]
     x, w = W.make()
     n = x.shape[0]
     plan = B.Plan(B.PointSet(W.d, x), W.leaf, B.parse_kernel_spec(W.kernel), W.sigma, W.m,
                   nrhs=W.nrhs, grid_mode=1 if args.scaled else 0,
-                  stencil_k=args.scaled if args.scaled else 10)
+                  stencil_k=args.scaled if args.scaled else 10,
+                  tuning=json.loads(args.tuning))
     lam = torch.from_numpy(np.ascontiguousarray(w.reshape(W.nrhs, n))).cuda()
     out = torch.empty_like(lam)
     s = torch.cuda.Stream()
@@ -42,7 +46,12 @@ def main():
             plan.execute_device(lam.data_ptr(), out.data_ptr(), stream=sp)
         e1.record(s)
     torch.cuda.synchronize()
-    print(f"{args.tag} {args.workload} ms/matvec {e0.elapsed_time(e1) / args.steps:.4f}", flush=True)
+    ms = e0.elapsed_time(e1) / args.steps
+    plan.set_profiling(True)
+    plan.execute_device(lam.data_ptr(), out.data_ptr(), stream=sp)
+    st = {k: round(v[0], 3) for k, v in plan.stage_times().items()}
+    print(f"{args.tag} {args.workload} ms/matvec {ms:.4f} stages {st} kernels {plan.kernels()}",
+          flush=True)
 
 
 if __name__ == "__main__":
