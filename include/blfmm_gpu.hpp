@@ -51,38 +51,26 @@ inline void check(int code) {
 }
 
 // Plan cache: the tree + grids a caller builds once are reused across
-// matvecs (the solver pattern, solver.cpp:280-293); a new point set, tree
-// depth or grid rebuilds the device plan.
-// Cheap identity of a point set's contents (sampled FNV-1a over the
-// coordinate bits): a new PointSet at a reused address, or coordinates
-// rewritten in place, rebuild the plan instead of hitting a stale one.
-inline std::uint64_t points_fingerprint(const PointSet& ps) {
-  std::uint64_t h = 1469598103934665603ull;
-  auto mix = [&](double v) {
-    std::uint64_t b;
-    std::memcpy(&b, &v, sizeof b);
-    h = (h ^ b) * 1099511628211ull;
-  };
-  const std::size_t n = ps.pts.size(), step = n > 4096 ? n / 4096 : 1;
-  for (std::size_t i = 0; i < n; i += step) {
-    mix(ps.pts[i][0]);
-    mix(ps.pts[i][1]);
-  }
-  if (n) {
-    mix(ps.pts[n - 1][0]);
-    mix(ps.pts[n - 1][1]);
-  }
-  mix(ps.domain.lo[0]);
-  mix(ps.domain.lo[1]);
-  mix(ps.domain.hi[0]);
-  mix(ps.domain.hi[1]);
-  return h;
+// matvecs (the solver pattern, solver.cpp:280-293). The reference recomputes
+// from req.ps on every call, so the cached plan is reused only when the FULL
+// coordinate array (and the domain) equals the copy the plan was built from:
+// a new PointSet at a reused address, or coordinates rewritten in place,
+// rebuild the plan instead of hitting a stale one.
+inline void flatten_points(const PointSet& ps, std::vector<double>& out) {
+  const int d = ps.d;
+  out.resize(ps.pts.size() * d + 4);
+  for (std::size_t i = 0; i < ps.pts.size(); ++i)
+    for (int q = 0; q < d; ++q) out[i * d + q] = ps.pts[i][q];
+  const std::size_t t = ps.pts.size() * d;
+  out[t] = ps.domain.lo[0];
+  out[t + 1] = ps.domain.lo[1];
+  out[t + 2] = ps.domain.hi[0];
+  out[t + 3] = ps.domain.hi[1];
 }
 
 struct PlanHandle {
   blfmm_plan* p = nullptr;
-  const PointSet* ps = nullptr;
-  std::uint64_t fp = 0;
+  std::vector<double> coords;  // flattened coordinates + domain the plan was built from
   std::size_t n = 0;
   int leaf = 0, m = 0, mode = 0, stencil = 10;
   double sigma = 0.0;
@@ -97,8 +85,9 @@ inline blfmm_plan* plan_for(const PointSet& ps, const BoxTree& tree, const Radia
                             double sigma, int m, const std::vector<double>& c_vals,
                             int mode = BLFMM_GRID_SHARED, int stencil_k = 10) {
   thread_local std::unique_ptr<PlanHandle> cache;
-  const std::uint64_t fp = points_fingerprint(ps);
-  if (cache && cache->ps == &ps && cache->fp == fp && cache->n == ps.pts.size() &&
+  thread_local std::vector<double> coords;
+  flatten_points(ps, coords);
+  if (cache && cache->n == ps.pts.size() && cache->coords == coords &&
       cache->leaf == tree.leaf_level &&
       cache->m == m && cache->sigma == sigma && cache->kernel.type == k.type &&
       cache->kernel.shape == k.shape && cache->c_vals == c_vals && cache->mode == mode &&
@@ -106,9 +95,6 @@ inline blfmm_plan* plan_for(const PointSet& ps, const BoxTree& tree, const Radia
     return cache->p;
   cache.reset(new PlanHandle());
   const int d = ps.d;
-  std::vector<double> coords(ps.pts.size() * d);
-  for (std::size_t i = 0; i < ps.pts.size(); ++i)
-    for (int q = 0; q < d; ++q) coords[i * d + q] = ps.pts[i][q];
   blfmm_plan_desc desc;
   std::memset(&desc, 0, sizeof(desc));
   desc.d = d;
@@ -130,8 +116,7 @@ inline blfmm_plan* plan_for(const PointSet& ps, const BoxTree& tree, const Radia
   desc.c_table = c_vals.data();  // the reference's own C(xi_m): bit-identical spectrum
   desc.world = 1;
   check(blfmm_plan_create(&desc, &cache->p));
-  cache->ps = &ps;
-  cache->fp = fp;
+  cache->coords = coords;
   cache->n = ps.pts.size();
   cache->leaf = tree.leaf_level;
   cache->m = m;

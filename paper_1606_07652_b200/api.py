@@ -438,24 +438,29 @@ class Plan:
 
 
 def _plan_for(req: SumRequest, tree: BoxTree, grids: LevelGrids, nrhs: int) -> Plan:
+    """The device plan of (point set, tree, grids), reused across matvecs (the
+    solver pattern, solver.cpp:280-293). The reference recomputes from
+    req.ps on every call, so a cached plan is only returned when the FULL
+    coordinate array equals the copy the plan was built from (coordinates
+    edited in place, or a new array at a recycled id, rebuild the plan)."""
     ps = req.ps
     cache = grids.__dict__.setdefault("_plans", {})
-    pts = np.asarray(ps.pts)
-    step = max(1, pts.shape[0] // 4096)
-    fp = hash(np.ascontiguousarray(pts[::step]).tobytes()) if pts.size else 0
-    key = (id(ps), id(ps.pts), ps.pts.shape, fp, tree.leaf_level, nrhs, req.kernel)
-    plan = cache.get(key)
-    if plan is None:
-        g = grids.grids[tree.leaf_level]
-        if grids.mode == GridMode.scaled:
-            ctab = np.concatenate([grids.factors[l].c_vals
-                                   for l in range(2, tree.leaf_level + 1)])
-        else:
-            ctab = grids.factors[tree.leaf_level].c_vals
-        plan = Plan(ps, tree.leaf_level, req.kernel, g.sigma, g.m_per_dim, c_table=ctab,
-                    nrhs=nrhs, grid_mode=int(grids.mode), stencil_k=grids.stencil_k)
-        cache.clear()
-        cache[key] = plan
+    pts = np.ascontiguousarray(np.asarray(ps.pts, dtype=np.float64))
+    key = (pts.shape, tree.leaf_level, nrhs, req.kernel,
+           tuple(ps.domain.lo), tuple(ps.domain.hi))
+    hit = cache.get(key)
+    if hit is not None and np.array_equal(hit[0], pts):
+        return hit[1]
+    g = grids.grids[tree.leaf_level]
+    if grids.mode == GridMode.scaled:
+        ctab = np.concatenate([grids.factors[l].c_vals
+                               for l in range(2, tree.leaf_level + 1)])
+    else:
+        ctab = grids.factors[tree.leaf_level].c_vals
+    plan = Plan(ps, tree.leaf_level, req.kernel, g.sigma, g.m_per_dim, c_table=ctab,
+                nrhs=nrhs, grid_mode=int(grids.mode), stencil_k=grids.stencil_k)
+    cache.clear()
+    cache[key] = (pts.copy(), plan)
     return plan
 
 

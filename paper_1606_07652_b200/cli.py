@@ -87,6 +87,7 @@ def read_points_csv(path: str, d: int):
 def cmd_fmm_matvec(a, cmdline: str) -> int:
     """blfmm_cli.cpp:353-413."""
     from . import api as B
+    from .solver import default_leaf_level
     k = B.parse_kernel_spec(a.kernel)
     ps = read_points_csv(a.points, infer_dimension(a.points))
     w = read_vector_csv(a.weights)
@@ -99,11 +100,11 @@ def cmd_fmm_matvec(a, cmdline: str) -> int:
     if a.mode == "direct":
         res = B.direct_matvec(k, ps, w, False, a.sigma)
     elif a.mode == "single":
-        level = a.levels if a.levels > 0 else max(2, _lround(0.5 * math.log2(float(n))))
+        level = a.levels if a.levels > 0 else default_leaf_level(n, ps.d, False)
         tree = B.build_tree(ps, level)
         res = B.fmm_matvec_single(B.SumRequest(k, a.sigma, ps, w, m), tree)
     else:
-        level = a.levels if a.levels > 0 else max(3, _lround(math.log2(float(n) / 32.0)))
+        level = a.levels if a.levels > 0 else default_leaf_level(n, ps.d, True)
         if level < 3:
             raise ValueError("mlfmm needs --levels >= 3")
         tree = B.build_tree(ps, level)

@@ -171,6 +171,22 @@ def run_gmres(apply, b, tol: float, max_iter: int):
     raise AccuracyError("gmres did not reach tolerance", best)
 
 
+def default_leaf_level(n: int, d: int, multilevel: bool) -> int:
+    """Leaf level when the caller gives none. d <= 2: the reference's rules
+    (multilevel lround(log2(n/32)), solver.cpp:280 / blfmm_cli.cpp:377-380;
+    single level lround(log2(sqrt n))), kept for parity. d = 3 (no reference
+    counterpart): the same targets counted in 8^L boxes - about 32 points per
+    leaf (multilevel) or sqrt(n) leaves (single level) - clamped to the
+    plan's d*L <= 24 box cap (geometry.cpp:266-267)."""
+    if d <= 2:
+        if multilevel:
+            return max(3, _lround(math.log2(float(n) / 32.0)))
+        return max(2, _lround(math.log2(math.sqrt(float(n)))))
+    if multilevel:
+        return min(8, max(3, _lround(math.log2(max(float(n) / 32.0, 1.0)) / 3.0)))
+    return min(8, max(2, _lround(math.log2(max(float(n), 1.0)) / 6.0)))
+
+
 def _lround(v: float) -> int:
     """std::lround: half away from zero (Python's round() is half-to-even)."""
     return int(math.floor(v + 0.5)) if v >= 0 else -int(math.floor(-v + 0.5))
@@ -218,13 +234,10 @@ def solve_interpolation(prob: InterpolationProblem):
             xv = x.detach().cpu().numpy()
             return torch.from_numpy(direct_matvec(prob.kernel, ps, xv).values).to(dev)
     elif prob.backend == Backend.single_fmm:
-        level = max(2, _lround(math.log2(math.sqrt(float(n)))))
-        level = prob.leaf_level if prob.leaf_level > 0 else level
+        level = prob.leaf_level if prob.leaf_level > 0 else default_leaf_level(n, ps.d, False)
         apply = _device_apply(Plan(ps, level, prob.kernel, sigma, m))
     else:
-        level = max(3, _lround(math.log2(float(n) / 32.0)))
-        if prob.leaf_level > 0:
-            level = prob.leaf_level
+        level = prob.leaf_level if prob.leaf_level > 0 else default_leaf_level(n, ps.d, True)
         apply = _device_apply(Plan(ps, level, prob.kernel, sigma, m))
     b = torch.from_numpy(rhs).to(dev)
     runner = run_cg if positive_definite(prob.kernel) else run_gmres

@@ -605,3 +605,26 @@ def test_stats_request_only_adds_the_imag_residual(blfmm):
     assert res[0] > 0 and all(r == res[0] for r in res)
     assert ref.stats.max_imag_residual == res[0]
     assert np.array_equal(ref.values, vals[0][0])
+
+
+def test_plan_cache_sees_in_place_coordinate_edits(blfmm):
+    """mlfmm_matvec reuses the device plan of an unchanged point set, but a
+    coordinate rewritten in place (off any sampling stride) must rebuild it:
+    the reference recomputes from req.ps on every call."""
+    B = blfmm
+    W = I.WORKLOADS["P3"]
+    x, w = W.make(20000)
+    x = np.array(x)
+    k = B.parse_kernel_spec(W.kernel)
+    ps = B.PointSet(3, x)
+    tree = B.build_tree(ps, 3)
+    grids = B.make_level_grids(k, W.sigma, W.m, 3, 3)
+    r1 = B.mlfmm_matvec(B.SumRequest(k, W.sigma, ps, w, W.m), tree, grids).values
+    r1b = B.mlfmm_matvec(B.SumRequest(k, W.sigma, ps, w, W.m), tree, grids).values
+    assert np.array_equal(r1, r1b)
+    ps.pts[12345] = [0.5, 0.5, 0.5]  # in place, same array object
+    r2 = B.mlfmm_matvec(B.SumRequest(k, W.sigma, ps, w, W.m), tree, grids).values
+    fresh = B.mlfmm_matvec(B.SumRequest(k, W.sigma, B.PointSet(3, ps.pts.copy()), w, W.m),
+                           B.build_tree(ps, 3), B.make_level_grids(k, W.sigma, W.m, 3, 3)).values
+    assert not np.array_equal(r1, r2)
+    assert np.array_equal(r2, fresh)

@@ -69,3 +69,18 @@ def test_gmres_on_mq_and_validation(blfmm):
         S.solve_interpolation(S.InterpolationProblem(k, ps, rhs[:-1]))
     with pytest.raises(blfmm.InvalidArgument):
         S.solve_interpolation(S.InterpolationProblem(k, ps, rhs, tol=0.0))
+
+
+def test_default_leaf_level_rules():
+    """d <= 2 keeps the reference's rules (blfmm_cli.cpp:377-380, solver.cpp);
+    d = 3 counts 8^L boxes and stays inside the d*L <= 24 cap."""
+    f = S.default_leaf_level
+    assert f(4096, 2, True) == max(3, S._lround(math.log2(4096 / 32.0)))
+    assert f(1 << 22, 2, True) == 17  # the reference's (1-D calibrated) value
+    assert f(4096, 2, False) == max(2, S._lround(math.log2(math.sqrt(4096.0))))
+    for n in (1000, 11_600, 100_000, 1 << 20, 1 << 24, 1 << 30):
+        for ml in (True, False):
+            L = f(n, 3, ml)
+            assert 3 * L <= 24 and L >= (3 if ml else 2)
+    # about 32 points per leaf
+    assert f(1 << 20, 3, True) == 5 and f(262_144, 3, True) == 4
