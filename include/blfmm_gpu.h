@@ -138,6 +138,9 @@ typedef struct blfmm_tuning {
   int near_ctas_per_sm; /* persistent near-field CTAs per SM (0: plan heuristic) */
   int near_reg_cap;     /* near-field register cap: 80, or 255 uncapped
                            (0: plan heuristic) */
+  int couple_tile;      /* telescoped 3-D leaf couple: 0 per-parent 4^3 regions
+                           (k_couple3<ROOT>), 1 z-streamed 2x2 column tiles
+                           (k_couple_col); -1: plan default (1) */
 } blfmm_tuning;
 
 /* Per-stage device times of the last execute (CUDA events on the launch

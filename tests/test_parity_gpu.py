@@ -504,7 +504,7 @@ def test_telescoped_equals_level_sweep(blfmm, oracle, name, n, leaf):
     for tv in (0, 1):
         r, plan = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf, tuning={"telescope": tv})
         assert plan.info().telescoped == tv
-        assert plan.kernels()["couple"] == ("k_root+k_couple3<ROOT>" if tv else "k_couple3")
+        assert plan.kernels()["couple"] == ("k_root+k_couple_col<2x2>" if tv else "k_couple3")
         res[tv] = r
     a, b = res[1], res[0]
     assert rel_l2(a.values, b.values) <= 1e-13, rel_l2(a.values, b.values)
@@ -628,3 +628,26 @@ def test_plan_cache_sees_in_place_coordinate_edits(blfmm):
                            B.build_tree(ps, 3), B.make_level_grids(k, W.sigma, W.m, 3, 3)).values
     assert not np.array_equal(r1, r2)
     assert np.array_equal(r2, fresh)
+
+
+@pytest.mark.parametrize("name,n,leaf", [("P3", 200000, 5), ("P3", 30000, 3), ("P5", 8192, 3),
+                                         ("P2p", 20000, 4)])
+def test_column_couple_equals_parent_regions(blfmm, oracle, name, n, leaf):
+    """The z-streamed column-tile leaf couple (k_couple_col, the default) and
+    the per-parent 4^3-region kernel (k_couple3<ROOT>) evaluate the same
+    telescoped L_L = e^{i xi (x_a - x_0)} C V_0 - C NS_L in a different
+    summation order: equal to rounding on sparse (blob) and dense trees, and
+    the default matches the oracle."""
+    W = I.WORKLOADS[name]
+    x, w = W.make(n)
+    if w.ndim == 2:
+        w = w[:4]
+    r0, p0 = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf, tuning={"couple_tile": 0})
+    r1, p1 = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
+    assert p0.kernels()["couple"] == "k_root+k_couple3<ROOT>"
+    assert p1.kernels()["couple"] == "k_root+k_couple_col<2x2>"
+    assert rel_l2(r1.values, r0.values) <= 1e-14, rel_l2(r1.values, r0.values)
+    ctab = blfmm.translation_coefficients(blfmm.parse_kernel_spec(W.kernel),
+                                          blfmm.make_quadrature(W.sigma, W.m, W.d)).c_vals
+    ov, _, _ = oracle.mlfmm(x, w, W.kernel, W.sigma, W.m, leaf, c_table_in=ctab)
+    assert rel_l2(r1.values, ov) <= TOL
