@@ -504,7 +504,7 @@ def test_telescoped_equals_level_sweep(blfmm, oracle, name, n, leaf):
     for tv in (0, 1):
         r, plan = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf, tuning={"telescope": tv})
         assert plan.info().telescoped == tv
-        assert plan.kernels()["couple"] == ("k_root+k_couple_col<2x2>" if tv else "k_couple3")
+        assert plan.kernels()["couple"] == ("k_root+k_couple_col<2x2,z32>" if tv else "k_couple3")
         res[tv] = r
     a, b = res[1], res[0]
     assert rel_l2(a.values, b.values) <= 1e-13, rel_l2(a.values, b.values)
@@ -645,7 +645,7 @@ def test_column_couple_equals_parent_regions(blfmm, oracle, name, n, leaf):
     r0, p0 = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf, tuning={"couple_tile": 0})
     r1, p1 = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, W.m, leaf)
     assert p0.kernels()["couple"] == "k_root+k_couple3<ROOT>"
-    assert p1.kernels()["couple"] == "k_root+k_couple_col<2x2>"
+    assert p1.kernels()["couple"] == "k_root+k_couple_col<2x2,z32>"
     assert rel_l2(r1.values, r0.values) <= 1e-14, rel_l2(r1.values, r0.values)
     ctab = blfmm.translation_coefficients(blfmm.parse_kernel_spec(W.kernel),
                                           blfmm.make_quadrature(W.sigma, W.m, W.d)).c_vals

@@ -75,7 +75,7 @@ def test_p3_full_size_matches_oracle(blfmm, oracle):
     plan = production_plan(blfmm, W, x)
     k = plan.kernels()
     assert k["p2m"] == "k_p2m_m2m_h16" and k["l2p"] == "k_l2p_h16S", k
-    assert k["couple"] == "k_root+k_couple_col<2x2>", k
+    assert k["couple"] == "k_root+k_couple_col<2x2,z32>", k
     assert k["near"] == "k_near_all(ctas_per_sm=2,regcap=80,sym_min=16)", k
     info = plan.info()
     assert info.near_sym_items > 0 and info.near_items > 0
@@ -119,7 +119,7 @@ def test_p2_full_size_matches_oracle_on_target_subset(blfmm, oracle):
     plan = production_plan(blfmm, W, x)
     k = plan.kernels()
     assert k["p2m"] == "k_p2m_mma" and k["l2p"] == "k_l2p_mma", k
-    assert k["couple"] == "k_root+k_couple_col<2x2>", k
+    assert k["couple"] == "k_root+k_couple_col<2x2,z32>", k
     assert k["near"].startswith("k_near_all(") and plan.info().near_sym_items > 0, k
     res = plan.execute(w)
     sel, mask = sample_leaves(oracle, x, W.leaf, 24, 2)
@@ -165,7 +165,7 @@ def test_p4_full_size_matches_reference(blfmm, oracle):
     x, w = W.make()
     plan = production_plan(blfmm, W, x)
     k = plan.kernels()
-    assert k["p2m"] == "k_p2m_mma" and k["couple"] == "k_couple" and k["l2p"] == "k_l2p_mma", k
+    assert k["p2m"] == "k_p2m_2d16" and k["couple"] == "k_couple" and k["l2p"] == "k_l2p_2d16", k
     assert k["near"] == "k_near_all(ctas_per_sm=3,regcap=none,sym_min=16)", k
     assert plan.info().near_sym_items > 0
     res = plan.execute(w)
