@@ -175,8 +175,9 @@ def run_ours(args, W, world, rank, local):
     t0 = time.perf_counter()
     sharded = None
     if world > 1:
-        # exchange mode: partitioned upsweep, NCCL all-reduce of the coarse
-        # expansions, downsweep, all-reduce of u (distributed.ShardedMatvec)
+        # the library's distributed execute (blfmm_plan_attach_nccl): partitioned
+        # upsweep, NCCL all-reduce of the level-1 expansions, owned downsweep +
+        # near field, NCCL broadcast gather of the owned slices of u
         from paper_1606_07652_b200 import distributed as Dst
         sharded = Dst.ShardedMatvec(B.PointSet(W.d, x), W.leaf, k, W.sigma, W.m, nrhs=nrhs,
                                     device=local, rank=rank, world=world)
@@ -277,10 +278,8 @@ def run_ours(args, W, world, rank, local):
     for _ in range(args.steps):
         if world == 1:
             e2e_call(B, plan, lam_np, out_np, sp)
-        else:  # sharded public API: H2D, matvec, all-reduce, D2H
-            lam.copy_(hl, non_blocking=True)
-            step()
-            ho.copy_(out, non_blocking=True)
+        else:  # sharded, same C ABI call: H2D, distributed matvec, D2H
+            e2e_call(B, plan, lam_np, out_np, sp)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = e0.elapsed_time(e1) / args.steps
@@ -369,7 +368,8 @@ def run_ours(args, W, world, rank, local):
                    "sigma": W.sigma, "m_per_dim": W.m, "K": K, "leaf_level": W.leaf,
                    "points": W.points, "grid_mode": "shared",
                    "parallelism": (f"morton-range x{world} (halo P2M + NCCL all-reduce of "
-                                   f"level-1 multipoles (telescoped) + all-reduce of u)")
+                                   f"level-1 multipoles (telescoped) + broadcast gather of "
+                                   f"the owned slices of u, inside libblfmm_gpu)")
                                   if world > 1 else "single",
                    "l2": "per-step working set (expansions %.1f GB) >> 126 MB L2" %
                          (info.device_bytes / 1e9),
@@ -378,8 +378,9 @@ def run_ours(args, W, world, rank, local):
                 "h2d_bytes_per_step": 8 * n * nrhs,
                 "d2h_bytes_per_step": 8 * n * nrhs,
                 "api": ("blfmm_execute (C ABI, host buffers, stats NULL)" if world == 1 else
-                        "ShardedMatvec: pinned H2D + upsweep + NCCL expansion all-reduce + "
-                        "downsweep + NCCL all-reduce of u + D2H")},
+                        "blfmm_execute on a plan with an NCCL communicator (C ABI, host "
+                        "buffers): H2D + upsweep + NCCL expansion all-reduce + downsweep + "
+                        "NCCL gather of u + D2H")},
         "ms_per_step_with_stats": ms_stats,
         "ms_per_step_level_sweep": ms_sweep,
         "kernels": plan.kernels(),

@@ -233,6 +233,37 @@ int blfmm_execute_upsweep(blfmm_plan* plan, const double* d_lambda, void* stream
 int blfmm_execute_downsweep(blfmm_plan* plan, double* d_out, blfmm_stats* stats,
                             void* stream);
 
+/* Multi-GPU inside the library (SURVEY §8e, §8b "Multi-GPU is internal to
+ * the plan"): attach a communicator to a world > 1 plan and blfmm_execute /
+ * blfmm_execute_device run the whole sharded matvec - upsweep (exchange
+ * mode) -> sum all-reduce of the upper-level expansion buffer -> downsweep
+ * and near field of the owned leaves -> gather of the owned slices of u
+ * (one broadcast per rank and right-hand side) -> u in the caller's order
+ * on every rank. lambda is the full vector on every rank (the reference's
+ * SumRequest::weights). Stats: max_imag_residual is max-reduced over ranks.
+ *
+ * NCCL: rank 0 calls blfmm_nccl_get_unique_id, the caller broadcasts the 128
+ * bytes (any channel), every rank calls blfmm_plan_attach_nccl on its plan
+ * (created with its rank / world / device). libnccl.so.2 is loaded on first
+ * use (dlopen); failures return BLFMM_ENCCL. Collectives are enqueued on the
+ * plan stream. A world = 1 plan accepts a one-rank communicator (same path,
+ * trivial collectives).
+ *
+ * blfmm_comm_ops: the same orchestration over caller-supplied collectives
+ * (MPI, a host transport, a test harness). Each callback receives a DEVICE
+ * pointer and the stream the data is ordered on, and returns 0 on success;
+ * it must leave the result in place before its stream work completes. */
+#define BLFMM_NCCL_ID_BYTES 128
+typedef struct blfmm_comm_ops {
+  void* ctx;
+  int (*all_reduce_sum)(void* ctx, double* d_buf, long long count, void* stream);
+  int (*all_reduce_max)(void* ctx, double* d_buf, long long count, void* stream);
+  int (*broadcast)(void* ctx, double* d_buf, long long count, int root, void* stream);
+} blfmm_comm_ops;
+int blfmm_nccl_get_unique_id(unsigned char id[BLFMM_NCCL_ID_BYTES]);
+int blfmm_plan_attach_nccl(blfmm_plan* plan, const unsigned char id[BLFMM_NCCL_ID_BYTES]);
+int blfmm_plan_attach_comm(blfmm_plan* plan, const blfmm_comm_ops* ops);
+
 /* Independent O(N^2) check (direct_matvec, fmm.cpp:30-75): values for
  * n_targets target indices (NULL = all n) into HOST out. */
 int blfmm_direct(int d, long long n, const double* coords, int kernel_type,

@@ -64,6 +64,20 @@ class Tuning(ct.Structure):
                 ("couple_tile", ct.c_int)]
 
 
+# blfmm_comm_ops callbacks: (ctx, device pointer, count, [root,] stream) -> 0 / error
+SUM_FN = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_longlong, ct.c_void_p)
+BCAST_FN = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_longlong, ct.c_int, ct.c_void_p)
+
+
+class CommOps(ct.Structure):
+    """blfmm_comm_ops (include/blfmm_gpu.h): caller-supplied collectives."""
+    _fields_ = [("ctx", ct.c_void_p), ("all_reduce_sum", SUM_FN), ("all_reduce_max", SUM_FN),
+                ("broadcast", BCAST_FN)]
+
+
+NCCL_ID_BYTES = 128
+
+
 class StageTimes(ct.Structure):
     _fields_ = [("ms", ct.c_double * NSTAGES), ("launches", ct.c_int * NSTAGES)]
 
@@ -101,6 +115,9 @@ EXPORTS = {
     "blfmm_execute_upsweep": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.c_void_p]),
     "blfmm_execute_downsweep": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.POINTER(Stats),
                                            ct.c_void_p]),
+    "blfmm_nccl_get_unique_id": (ct.c_int, [ct.c_char_p]),
+    "blfmm_plan_attach_nccl": (ct.c_int, [ct.c_void_p, ct.c_char_p]),
+    "blfmm_plan_attach_comm": (ct.c_int, [ct.c_void_p, ct.POINTER(CommOps)]),
     "blfmm_direct": (ct.c_int, [ct.c_int, ct.c_longlong, ct.POINTER(ct.c_double), ct.c_int,
                                 ct.c_double, ct.POINTER(ct.c_double), ct.c_longlong,
                                 ct.POINTER(ct.c_longlong), ct.POINTER(ct.c_double), ct.c_int]),

@@ -397,6 +397,32 @@ class Plan:
         return None
 
     # ---- multi-GPU exchange mode (blfmm_execute_upsweep / _downsweep)
+    def attach_nccl(self, unique_id: bytes):
+        """Attach an NCCL communicator (rank / world of this plan): execute
+        then runs the whole sharded matvec and returns u on every rank."""
+        if len(unique_id) != _capi.NCCL_ID_BYTES:
+            raise InvalidArgument("NCCL unique id must be 128 bytes")
+        _capi.check(_capi.lib().blfmm_plan_attach_nccl(self._h, unique_id))
+
+    def attach_comm(self, all_reduce_sum, all_reduce_max, broadcast):
+        """Attach caller collectives: all_reduce_sum(dptr, count, stream),
+        all_reduce_max(dptr, count, stream), broadcast(dptr, count, root,
+        stream), each on a device buffer of float64, returning None."""
+        def wrap(f):
+            def cb(_ctx, *a):
+                try:
+                    f(*a)
+                    return 0
+                except Exception:  # noqa: BLE001 - reported as BLFMM_ENCCL
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            return cb
+        self._ops = _capi.CommOps(None, _capi.SUM_FN(wrap(all_reduce_sum)),
+                                  _capi.SUM_FN(wrap(all_reduce_max)),
+                                  _capi.BCAST_FN(wrap(broadcast)))
+        _capi.check(_capi.lib().blfmm_plan_attach_comm(self._h, ct.byref(self._ops)))
+
     def exchange_size(self) -> int:
         """Doubles in the exchange buffer (0: no exchange mode)."""
         v = ct.c_longlong()
@@ -435,6 +461,13 @@ class Plan:
         _capi.check(_capi.lib().blfmm_get_expansions(self._h, level, kind, rhs, _ptr(out)))
         z = out.reshape(cnt, self.K, 2)
         return z[..., 0] + 1j * z[..., 1]
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0; broadcast it to the others)."""
+    buf = ct.create_string_buffer(_capi.NCCL_ID_BYTES)
+    _capi.check(_capi.lib().blfmm_nccl_get_unique_id(buf))
+    return buf.raw
 
 
 def _plan_for(req: SumRequest, tree: BoxTree, grids: LevelGrids, nrhs: int) -> Plan:

@@ -1,7 +1,9 @@
-"""Multi-rank path on CPU (gloo, world_size 2): the host-side sharding logic
-the GPU ranks use — the deterministic Morton-range partition (blfmm_partition,
-host-only code of the C-ABI library) and the all-reduce assembly of disjoint
-partial outputs — with the CPU oracle standing in for each rank's kernels."""
+"""Multi-rank path on CPU (gloo, world_size 2 and 3): the host-side sharding
+logic the GPU ranks use - the deterministic Morton-range partition
+(blfmm_partition, host-only code of the C-ABI library) and the gather of the
+ranks' owned slices of u (one broadcast per rank, as blfmm_execute does on a
+plan with a communicator) - with the CPU oracle standing in for each rank's
+kernels."""
 import math
 import os
 import socket
@@ -64,12 +66,16 @@ def _worker(rank, world, port, result_path):
     owned = np.concatenate([pts[b] for b in leaves[bounds[rank]:bounds[rank + 1]]] or
                            [np.zeros(0, dtype=np.int64)])
     full, _, _ = po.mlfmm(x, w, W.kernel, W.sigma, M, L)
-    local = np.zeros_like(full)
-    local[owned] = full[owned]  # this rank's kernels write only owned targets
-    t = torch.from_numpy(local)
-    D.assemble(t)
+    # gather: rank q broadcasts its owned slice (known sizes on every rank)
+    u = np.full_like(full, np.nan)
+    for q in range(world):
+        own_q = np.concatenate([pts[b] for b in leaves[bounds[q]:bounds[q + 1]]] or
+                               [np.zeros(0, dtype=np.int64)])
+        buf = torch.from_numpy(full[own_q].copy() if q == rank else np.zeros(len(own_q)))
+        dist.broadcast(buf, src=q)
+        u[own_q] = buf.numpy()
     if rank == 0:
-        np.savez(result_path, assembled=t.numpy(), full=full, bounds=bounds,
+        np.savez(result_path, assembled=u, full=full, bounds=bounds,
                  counts=np.array([len(owned)]))
     dist.destroy_process_group()
 
@@ -82,13 +88,14 @@ def free_port():
     return p
 
 
-def test_two_rank_partition_and_assembly(tmp_path, oracle):
+@pytest.mark.parametrize("world", [2, 3])
+def test_partition_and_owned_slice_gather(tmp_path, oracle, world):
     out = str(tmp_path / "r.npz")
-    mp.spawn(_worker, args=(2, free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, free_port(), out), nprocs=world, join=True)
     r = np.load(out)
-    assert np.array_equal(r["assembled"], r["full"])  # disjoint supports: exact
+    assert np.array_equal(r["assembled"], r["full"])  # every target owned once: exact
     b = r["bounds"]
-    assert b[0] == 0 and b[-1] > b[1] > 0
+    assert b[0] == 0 and np.all(np.diff(b) > 0)
 
 
 def test_partition_properties(oracle):
