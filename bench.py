@@ -355,6 +355,21 @@ def run_ours(args, W, world, rank, local):
                             "traffic": load_traffic(kern),
                             ("algorithmic_bytes" if unit == "GB/s" else "algorithmic_flops"): amount,
                             "peak_source": src, "ms": round(t_ms, 4)}
+        if unit == "TFLOP/s":
+            # reference-equivalent work (the reference's full-grid / ordered-pair
+            # count) vs the FP64 work the kernel executes (half spectrum,
+            # symmetric pairs, operand formation), from the committed ncu
+            # capture of one matvec: physical rate = this run's time x the
+            # capture's physical / algorithmic ratio
+            ph = load_physical(kern)
+            if ph:
+                phys = ph["flops"] / (t_ms / 1e3) / 1e12
+                stage_roof[name]["physical"] = {
+                    "executed_fp64_flops": ph["flops"], "achieved": round(phys, 2),
+                    "frac": round(phys / peak_v, 4),
+                    "fp64_pipe_pct": ph.get("fp64_pipe_pct"),
+                    "dmma_pipe_pct": ph.get("dmma_pipe_pct"),
+                    "source": os.path.relpath(TRAFFIC_PROFILE, ROOT)}
     roof = None
     if top in stage_roof:
         roof = dict(stage_roof[top], dominant_stage=top)
@@ -473,7 +488,7 @@ def ct_stream(stream):
     return ct.c_void_p(stream.cuda_stream)
 
 
-TRAFFIC_PROFILE = os.path.join(ROOT, "profiles", "r01_ncu_step_dram.json")
+TRAFFIC_PROFILE = os.path.join(ROOT, "profiles", "r02_ncu_step_metrics.json")
 
 
 def load_traffic(prefix):
@@ -485,6 +500,27 @@ def load_traffic(prefix):
             s = json.load(f)
         hits = [v["dram_bytes_total"] for k_, v in s["kernels"].items() if k_.startswith(prefix)]
         return float(sum(hits)) if hits else None
+    except Exception:
+        return None
+
+
+def load_physical(prefix):
+    """Executed FP64 work of the kernels whose name starts with `prefix` in the
+    committed one-matvec ncu capture: physical flops (DMMA m8n8k4 = 512, DFMA
+    = 2, DADD / DMUL = 1), the capture's kernel time, and the FP64 / DMMA
+    pipe utilisation (time-weighted), or None."""
+    try:
+        with open(TRAFFIC_PROFILE) as f:
+            s = json.load(f)
+        hits = [v for k_, v in s["kernels"].items() if k_.startswith(prefix)]
+        if not hits or not all("fp64_flops_physical" in v for v in hits):
+            return None
+        ms = sum(v["ms_total"] for v in hits)
+        out = {"flops": sum(v["fp64_flops_physical"] for v in hits), "ncu_ms": ms}
+        for key in ("fp64_pipe_pct", "dmma_pipe_pct"):
+            if all(key in v for v in hits):
+                out[key] = round(sum(v[key] * v["ms_total"] for v in hits) / max(ms, 1e-12), 2)
+        return out
     except Exception:
         return None
 
