@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--scaled", type=int, default=0, help="GridMode::scaled with this stencil")
+    ap.add_argument("--stats", type=int, default=0,
+                    help="request SumStats (the L2P imaginary-residual GEMM runs)")
     args = ap.parse_args()
     W = I.WORKLOADS[args.workload]
     x, w = W.make(args.n)
@@ -35,7 +37,7 @@ def main():
     sp = ct.c_void_p(s.cuda_stream)
     plan.set_profiling(True)
     for i in range(args.steps):
-        st = plan.execute_device(lam.data_ptr(), out.data_ptr(), stream=sp, stats=True)
+        st = plan.execute_device(lam.data_ptr(), out.data_ptr(), stream=sp, stats=args.stats)
         print(i, {k: round(v[0], 3) for k, v in plan.stage_times().items()}, flush=True)
     torch.cuda.synchronize()
 
