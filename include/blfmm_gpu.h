@@ -141,6 +141,10 @@ typedef struct blfmm_tuning {
   int couple_tile;      /* telescoped 3-D leaf couple: 0 per-parent 4^3 regions
                            (k_couple3<ROOT>), 1 z-streamed 2x2 column tiles
                            (k_couple_col); -1: plan default (1) */
+  int rhs_gemm;         /* 3-D M = 16 with >= 8 right-hand sides: P2M / L2P as
+                           real-weight DMMA GEMMs over all right-hand sides
+                           (k_p2m_mr / k_l2p_mr); 0: one right-hand side per
+                           CTA (k_p2m_m2m_h16 / k_l2p_h16S); -1: default (1) */
 } blfmm_tuning;
 
 /* Per-stage device times of the last execute (CUDA events on the launch

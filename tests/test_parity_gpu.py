@@ -651,3 +651,31 @@ def test_column_couple_equals_parent_regions(blfmm, oracle, name, n, leaf):
                                           blfmm.make_quadrature(W.sigma, W.m, W.d)).c_vals
     ov, _, _ = oracle.mlfmm(x, w, W.kernel, W.sigma, W.m, leaf, c_table_in=ctab)
     assert rel_l2(r1.values, ov) <= TOL
+
+
+@pytest.mark.parametrize("name,n,leaf,nr", [("P5", 20000, 3, 32), ("P5", 8192, 3, 8),
+                                            ("P3", 40000, 4, 12), ("P2p", 30000, 4, 40)])
+def test_rhs_gemm_matches_per_rhs_path_and_oracle(blfmm, oracle, name, n, leaf, nr):
+    """nrhs >= 8 with the 3-D half spectrum: P2M / L2P as real-weight DMMA
+    GEMMs over the right-hand sides (k_p2m_mr / k_l2p_mr; spans of 64 points,
+    partial right-hand-side groups, leaves of more than 64 points, blob
+    trees) against the one-right-hand-side-per-CTA kernels (tuning rhs_gemm
+    0) and the oracle; the imaginary residual (stats GEMM) too."""
+    W = I.WORKLOADS[name]
+    x, w0 = W.make(n)
+    w0 = w0 if w0.ndim == 1 else w0[0]
+    rng = np.random.default_rng(3)
+    w = np.ascontiguousarray(np.stack([w0] + [rng.uniform(-1, 1, w0.shape[0]) for _ in range(nr - 1)]))
+    ps = blfmm.PointSet(3, x)
+    k = blfmm.parse_kernel_spec(W.kernel)
+    pg = blfmm.Plan(ps, leaf, k, W.sigma, W.m, nrhs=nr)
+    p0 = blfmm.Plan(ps, leaf, k, W.sigma, W.m, nrhs=nr, tuning={"rhs_gemm": 0})
+    assert pg.kernels()["p2m"] == "k_p2m_mr" and pg.kernels()["l2p"] == "k_l2p_mr"
+    assert p0.kernels()["p2m"] != "k_p2m_mr"
+    rg, r0 = pg.execute(w), p0.execute(w)
+    assert rel_l2(rg.values, r0.values) <= 1e-13, rel_l2(rg.values, r0.values)
+    assert abs(rg.stats.max_imag_residual - r0.stats.max_imag_residual) <= \
+        1e-9 * max(1.0, r0.stats.max_imag_residual)
+    ctab = blfmm.translation_coefficients(k, blfmm.make_quadrature(W.sigma, W.m, 3)).c_vals
+    ov, _, _ = oracle.mlfmm(x, w[[0, nr - 1]], W.kernel, W.sigma, W.m, leaf, c_table_in=ctab)
+    assert rel_l2(rg.values[0], ov[0]) <= TOL and rel_l2(rg.values[nr - 1], ov[1]) <= TOL

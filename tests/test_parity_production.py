@@ -134,7 +134,8 @@ def test_p2_full_size_matches_oracle_on_target_subset(blfmm, oracle):
 def test_p5_full_size_batched_matches_oracle_on_target_subset(blfmm, oracle):
     """BASELINE configs[4]: 3-D Gaussian c=64 on the jittered 64x64x128 lattice
     (N=524,288, 128 points per leaf), 32 right-hand sides in one execute: the
-    half-spectrum DMMA P2M / L2P with 32 RHS and the batched near field
+    real-weight DMMA GEMMs over the 32 right-hand sides for P2M / L2P
+    (k_p2m_mr / k_l2p_mr, phases generated in shared memory) and the batched near field
     (k_near_dmma) - right-hand sides 0, 13 and 31 against the oracle on 16
     seeded target leaves."""
     W = I.WORKLOADS["P5"]
@@ -142,7 +143,7 @@ def test_p5_full_size_batched_matches_oracle_on_target_subset(blfmm, oracle):
     assert w.shape == (32, 524288)
     plan = production_plan(blfmm, W, x)
     k = plan.kernels()
-    assert k["p2m"] == "k_p2m_m2m_h16" and k["l2p"] == "k_l2p_h16S", k
+    assert k["p2m"] == "k_p2m_mr" and k["l2p"] == "k_l2p_mr", k
     assert k["near"] == "k_near_dmma", k
     res = plan.execute(w)
     rhs = [0, 13, 31]
