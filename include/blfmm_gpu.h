@@ -268,6 +268,26 @@ int blfmm_nccl_get_unique_id(unsigned char id[BLFMM_NCCL_ID_BYTES]);
 int blfmm_plan_attach_nccl(blfmm_plan* plan, const unsigned char id[BLFMM_NCCL_ID_BYTES]);
 int blfmm_plan_attach_comm(blfmm_plan* plan, const blfmm_comm_ops* ops);
 
+/* Krylov caller (solve_interpolation's iteration, solver.cpp:43-203, 269-300):
+ * solves A x = b with A the plan's matvec (one right-hand side), CG
+ * (BLFMM_SOLVE_CG, symmetric positive definite kernels) or GMRES restarted
+ * every 300 iterations (BLFMM_SOLVE_GMRES), the reference's recurrences and
+ * stopping rules; the vectors stay on the device, reductions are
+ * deterministic. b / x are HOST arrays in the caller's point order. Not
+ * reaching tol returns BLFMM_EACCURACY with the best relative residual in
+ * blfmm_last_error_value (the reference's accuracy_error), stats filled. */
+#define BLFMM_SOLVE_CG 1
+#define BLFMM_SOLVE_GMRES 2
+typedef struct blfmm_solve_stats {
+  int method;       /* BLFMM_SOLVE_CG / BLFMM_SOLVE_GMRES */
+  int iterations;
+  int matvecs;
+  int converged;
+  double residual;  /* relative residual (best seen if not converged) */
+} blfmm_solve_stats;
+int blfmm_solve(blfmm_plan* plan, int method, const double* b, double* x, double tol,
+                int max_iter, blfmm_solve_stats* stats);
+
 /* Independent O(N^2) check (direct_matvec, fmm.cpp:30-75): values for
  * n_targets target indices (NULL = all n) into HOST out. */
 int blfmm_direct(int d, long long n, const double* coords, int kernel_type,

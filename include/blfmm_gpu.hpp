@@ -20,11 +20,14 @@
 // (std::invalid_argument, std::domain_error, blfmm::accuracy_error).
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "blfmm/mlfmm.hpp"
@@ -224,6 +227,72 @@ inline SumResult direct_matvec(const RadialKernel& k, const PointSet& ps,
                      n, nullptr, res.values.data(), -1));
   res.stats.near_pairs = static_cast<long long>(n) * n;
   return res;
+}
+
+// solve_interpolation (solver.cpp:269-300, solver.hpp:16-46) without Eigen:
+// the Krylov loop runs in the library (blfmm_solve, device vectors) over the
+// multilevel plan of the problem's points (Backend::mlfmm, leaf level
+// lround(log2(N/32)) >= 3 unless given) or the single-level tree
+// (Backend::single_fmm, lround(log2(sqrt N)) >= 2; shared grids make the
+// multilevel sweep equal to the single-level sum to rounding). CG for the
+// positive definite kernels (kernels.cpp:334-337), restarted GMRES otherwise.
+// Backend::dense needs the reference's Eigen assembly and is refused.
+enum class Backend { dense, single_fmm, mlfmm };
+struct InterpolationProblem {
+  RadialKernel kernel;
+  const PointSet* ps = nullptr;
+  std::vector<double> rhs;
+  Backend backend = Backend::mlfmm;
+  double tol = 1e-10;
+  int max_iter = 2000;
+  double sigma = 0.0;  // <= 0: pi
+  int m_per_dim = 0;   // <= 0: choose_truncation(N)
+  int leaf_level = 0;  // 0: from N
+};
+struct SolveStats {
+  int iterations = 0;
+  double residual = 0.0;
+  long long matvecs = 0;
+  std::string method;
+  bool converged = false;
+};
+
+inline std::pair<std::vector<double>, SolveStats> solve_interpolation(
+    const InterpolationProblem& prob) {
+  if (!prob.ps) throw std::invalid_argument("problem has no point set");
+  const PointSet& ps = *prob.ps;
+  const int n = ps.size();
+  if (prob.rhs.size() != static_cast<std::size_t>(n))
+    throw std::invalid_argument("rhs length != point count");
+  if (!(prob.tol > 0.0)) throw std::invalid_argument("tol must be positive");
+  if (prob.backend == Backend::dense)
+    throw std::domain_error("dense backend needs the reference's Eigen assembly");
+  const double sigma = prob.sigma > 0.0 ? prob.sigma : 3.14159265358979323846;
+  const int m = prob.m_per_dim > 0 ? prob.m_per_dim : choose_truncation(n);
+  int level;
+  if (prob.backend == Backend::single_fmm) {
+    level = std::max(2, static_cast<int>(std::lround(std::log2(std::sqrt(static_cast<double>(n))))));
+    if (prob.leaf_level > 0) level = prob.leaf_level;
+  } else {
+    level = std::max(3, static_cast<int>(std::lround(std::log2(static_cast<double>(n) / 32.0))));
+    if (prob.leaf_level > 0) level = prob.leaf_level;
+  }
+  BoxTree tree = build_tree(ps, level);
+  LevelGrids grids = make_level_grids(prob.kernel, sigma, m, ps.d, level, GridMode::shared, 10);
+  blfmm_plan* p = plan_for(ps, tree, prob.kernel, sigma, m, grids.factors[level].c_vals);
+  const bool pd = prob.kernel.type == KernelType::Gaussian || prob.kernel.type == KernelType::IMQ;
+  std::vector<double> x(n, 0.0);
+  blfmm_solve_stats st{};
+  const int rc = blfmm_solve(p, pd ? BLFMM_SOLVE_CG : BLFMM_SOLVE_GMRES, prob.rhs.data(),
+                             x.data(), prob.tol, prob.max_iter, &st);
+  SolveStats out;
+  out.iterations = st.iterations;
+  out.residual = st.residual;
+  out.matvecs = st.matvecs;
+  out.method = st.method == BLFMM_SOLVE_CG ? "cg" : "gmres";
+  out.converged = st.converged != 0;
+  check(rc);  // BLFMM_EACCURACY -> accuracy_error (best residual), as the reference
+  return {std::move(x), out};
 }
 
 }  // namespace gpu

@@ -76,6 +76,13 @@ class CommOps(ct.Structure):
 
 
 NCCL_ID_BYTES = 128
+SOLVE_CG, SOLVE_GMRES = 1, 2
+
+
+class SolveStatsC(ct.Structure):
+    """blfmm_solve_stats (include/blfmm_gpu.h)."""
+    _fields_ = [("method", ct.c_int), ("iterations", ct.c_int), ("matvecs", ct.c_int),
+                ("converged", ct.c_int), ("residual", ct.c_double)]
 
 
 class StageTimes(ct.Structure):
@@ -116,6 +123,9 @@ EXPORTS = {
     "blfmm_execute_downsweep": (ct.c_int, [ct.c_void_p, ct.c_void_p, ct.POINTER(Stats),
                                            ct.c_void_p]),
     "blfmm_nccl_get_unique_id": (ct.c_int, [ct.c_char_p]),
+    "blfmm_solve": (ct.c_int, [ct.c_void_p, ct.c_int, ct.POINTER(ct.c_double),
+                               ct.POINTER(ct.c_double), ct.c_double, ct.c_int,
+                               ct.POINTER(SolveStatsC)]),
     "blfmm_plan_attach_nccl": (ct.c_int, [ct.c_void_p, ct.c_char_p]),
     "blfmm_plan_attach_comm": (ct.c_int, [ct.c_void_p, ct.POINTER(CommOps)]),
     "blfmm_direct": (ct.c_int, [ct.c_int, ct.c_longlong, ct.POINTER(ct.c_double), ct.c_int,

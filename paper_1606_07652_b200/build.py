@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libblfmm_gpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 HOST_CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["blfmm.cu"]
+CU_SOURCES = ["blfmm.cu", "krylov.cu"]
 CPP_SOURCES = ["spectrum.cpp"]
 
 

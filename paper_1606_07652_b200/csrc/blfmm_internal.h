@@ -22,6 +22,9 @@ struct KernelSpec {
 };
 
 KernelSpec parse_spec(const std::string& spec);
+// thread-local error state behind blfmm_last_error / blfmm_last_error_value
+void set_error(const Error& e);
+void set_error_message(const char* msg);
 void require_fmm_kernel(const KernelSpec& k);
 double fourier_value(const KernelSpec& k, double xi, int d);
 std::vector<double> translation_spectrum(const KernelSpec& k, double sigma,

@@ -17,6 +17,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import _capi
+
 from .api import (AccuracyError, InvalidArgument, KernelType, Plan, PointSet, RadialKernel,
                   choose_truncation, direct_matvec)
 
@@ -228,18 +230,38 @@ def solve_interpolation(prob: InterpolationProblem):
         raise InvalidArgument("tol must be positive")
     sigma = prob.sigma if prob.sigma > 0.0 else math.pi
     m = prob.m_per_dim if prob.m_per_dim > 0 else choose_truncation(n)
+    if prob.backend != Backend.dense:
+        # the Krylov loop runs in the C++ library (blfmm_solve: device vectors,
+        # the plan's matvec, deterministic reductions)
+        multilevel = prob.backend == Backend.mlfmm
+        level = prob.leaf_level if prob.leaf_level > 0 else default_leaf_level(n, ps.d, multilevel)
+        plan = Plan(ps, level, prob.kernel, sigma, m)
+        return solve_on_plan(plan, rhs, prob.tol, prob.max_iter, positive_definite(prob.kernel))
     dev = torch.device("cuda")
-    if prob.backend == Backend.dense:
-        def apply(x):
-            xv = x.detach().cpu().numpy()
-            return torch.from_numpy(direct_matvec(prob.kernel, ps, xv).values).to(dev)
-    elif prob.backend == Backend.single_fmm:
-        level = prob.leaf_level if prob.leaf_level > 0 else default_leaf_level(n, ps.d, False)
-        apply = _device_apply(Plan(ps, level, prob.kernel, sigma, m))
-    else:
-        level = prob.leaf_level if prob.leaf_level > 0 else default_leaf_level(n, ps.d, True)
-        apply = _device_apply(Plan(ps, level, prob.kernel, sigma, m))
+
+    def apply(x):
+        xv = x.detach().cpu().numpy()
+        return torch.from_numpy(direct_matvec(prob.kernel, ps, xv).values).to(dev)
     b = torch.from_numpy(rhs).to(dev)
     runner = run_cg if positive_definite(prob.kernel) else run_gmres
     x, stats = runner(apply, b, prob.tol, prob.max_iter)
     return x.cpu().numpy(), stats
+
+
+def solve_on_plan(plan: Plan, rhs, tol: float, max_iter: int, spd: bool):
+    """blfmm_solve: CG (spd) or restarted GMRES on the plan's matvec, in the
+    library. Returns (x, SolveStats); raises AccuracyError (best residual) when
+    the tolerance is not reached, as the reference."""
+    import ctypes as ct
+    rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+    x = np.zeros_like(rhs)
+    st = _capi.SolveStatsC()
+    rc = _capi.lib().blfmm_solve(plan.handle, _capi.SOLVE_CG if spd else _capi.SOLVE_GMRES,
+                                 rhs.ctypes.data_as(ct.POINTER(ct.c_double)),
+                                 x.ctypes.data_as(ct.POINTER(ct.c_double)), float(tol),
+                                 int(max_iter), ct.byref(st))
+    stats = SolveStats(iterations=st.iterations, residual=st.residual, matvecs=st.matvecs,
+                       method="cg" if st.method == _capi.SOLVE_CG else "gmres",
+                       converged=bool(st.converged))
+    _capi.check(rc)
+    return x, stats

@@ -311,7 +311,9 @@ def test_sharded_plans_assemble_to_full(blfmm, name, n, leaf):
 def test_cpp_adapter_dropin_against_reference():
     """include/blfmm_gpu.hpp + the reference library (built from its own
     sources) in one C++ program: the GPU matvec on the reference's own
-    PointSet / BoxTree / LevelGrids equals the reference's mlfmm_matvec."""
+    PointSet / BoxTree / LevelGrids equals the reference's mlfmm_matvec, and
+    the adapter's solve_interpolation (the library Krylov loop, blfmm_solve)
+    reproduces the reference's CG recurrence run with the reference matvec."""
     import json
     import subprocess
     exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref",
@@ -320,7 +322,8 @@ def test_cpp_adapter_dropin_against_reference():
         pytest.skip("oracle/_ref/adapter_parity not built (needs /root/reference at build time)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
-    assert len(lines) >= 7, r.stdout + r.stderr
+    assert len(lines) >= 9, r.stdout + r.stderr
+    assert sum(1 for l in lines if l["case"].startswith("solve")) == 2
     assert r.returncode == 0 and all(l["ok"] for l in lines), r.stdout
 
 

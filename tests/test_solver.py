@@ -84,3 +84,36 @@ def test_default_leaf_level_rules():
             assert 3 * L <= 24 and L >= (3 if ml else 2)
     # about 32 points per leaf
     assert f(1 << 20, 3, True) == 5 and f(262_144, 3, True) == 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,spec,n,leaf,spd", [("P2p", "gaussian:c=16000", 20000, 4, True),
+                                                   ("P2p", "gaussian:c=16000", 20000, 4, False),
+                                                   ("P4", "gaussian:c=400000", 30000, 5, False)])
+def test_library_krylov_matches_host_loop(blfmm, name, spec, n, leaf, spd):
+    """blfmm_solve (the CG / restarted-GMRES iteration of solver.cpp:43-203
+    inside the C++ library, device vectors) against the same recurrences
+    driven from Python on the same plan (narrow Gaussians on the P2 / P4
+    uniform point sets: FMM operators that CG / GMRES solve to 1e-8 in 80-300
+    iterations): the same iterates up to the
+    reduction order; non-convergence raises AccuracyError with the best
+    residual (accuracy_error)."""
+    W = I.WORKLOADS[name]
+    x, _ = W.make(n)
+    ps = blfmm.PointSet(W.d, x)
+    k = blfmm.parse_kernel_spec(spec)
+    plan = blfmm.Plan(ps, leaf, k, W.sigma, W.m)
+    rhs = np.cos(3 * x[:, 0]) * (1 + x[:, 1])
+    tol = 1e-8
+    xl, st = S.solve_on_plan(plan, rhs, tol, 400, spd)
+    assert st.converged and st.method == ("cg" if spd else "gmres")
+    b = torch.from_numpy(rhs).cuda()
+    runner = S.run_cg if spd else S.run_gmres
+    xh, sh = runner(S._device_apply(plan), b, tol, 400)
+    assert abs(st.iterations - sh.iterations) <= 2
+    assert np.linalg.norm(xl - xh.cpu().numpy()) <= 1e-6 * np.linalg.norm(xl)
+    u = plan.execute(xl).values
+    assert np.linalg.norm(u - rhs) <= 1.01 * tol * np.linalg.norm(rhs)
+    with pytest.raises(blfmm.AccuracyError) as e:
+        S.solve_on_plan(plan, rhs, 1e-15, 3, spd)
+    assert e.value.achieved > 1e-15

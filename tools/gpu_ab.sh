@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-for wl in P5; do timeout 300 python tools/time_step.py --workload $wl --steps 5 >> gpurun_out/steps.txt 2>&1; done
-timeout 1500 python -m pytest tests -m gpu -x -q -k "batched or P5 or p5 or rhs or distributed or nccl" > gpurun_out/pytest_sub.txt 2>&1; echo "exit $?" >> gpurun_out/pytest_sub.txt
+timeout 1500 python -m pytest tests -m gpu -x -q -k "solve or krylov or adapter or cli" > gpurun_out/pytest_sub.txt 2>&1; echo "exit $?" >> gpurun_out/pytest_sub.txt
+./oracle/_ref/adapter_parity > gpurun_out/adapter.txt 2>&1; echo "exit $?" >> gpurun_out/adapter.txt
