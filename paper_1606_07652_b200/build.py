@@ -22,8 +22,9 @@ CPP_SOURCES = ["spectrum.cpp"]
 
 
 def _sources():
+    import glob
     return [os.path.join(CSRC, f) for f in CU_SOURCES + CPP_SOURCES + [
-        "blfmm_internal.h", "device.cuh"]] + [
+        "blfmm_internal.h", "device.cuh"]] + sorted(glob.glob(os.path.join(CSRC, "*.inc.cuh"))) + [
         os.path.join(HERE, "..", "include", "blfmm_gpu.h")]
 
 

@@ -1,11 +1,11 @@
 // Host plan-time math of the band-limited FMM: kernel-spec grammar, closed
 // form spectra and the translation spectrum C(xi_m) on the uniform
 // left-endpoint grid. Everything here runs once per plan; the per-matvec hot
-// path is the CUDA code in far.cu / near.cu.
+// path is the CUDA code in blfmm.cu and its k_*.inc.cuh fragments.
 //
 // Reference behaviour followed:
 //   parse_kernel_spec      kernels.cpp:48-103
-//   eval_kernel            kernels.cpp:131-161 (device copy in blfmm_device.cuh)
+//   eval_kernel            kernels.cpp:131-161 (device copy: device.cuh phi_of_r2)
 //   eval_fourier           kernels.cpp:190-238; d = 3 from the same
 //                          (r^2+c^2)^{-beta} family
 //   make_quadrature        bandlimit.cpp:269-292 (row-major tensor nodes)
