@@ -128,3 +128,61 @@ def test_solve_writes_converged_coefficients(tmp_path, fixture_files):
                           "--out", str(lam)], tmp_path)
     assert rc == 1
     assert '"achieved"' in err and err.count("\n") == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim", [1, 2])
+def test_fmm_matvec_outputs_match_reference(tmp_path, oracle, dim):
+    """The CLI's artifacts against the REFERENCE library (compiled from its
+    sources; the oracle restatement where it is absent): u of every mode
+    (direct / single / mlfmm, rel-l2 <= 1e-10 against direct_matvec /
+    fmm_matvec_single / mlfmm_matvec on the same tight-bounds domain), the
+    near_pairs / far_work header lines, and the --dump-expansions multipoles
+    in reference box order (upsweep, mlfmm.cpp:201-266)."""
+    n = 512 if dim == 1 else 1024
+    x = np.stack([I.generate_quasiuniform(n, 1, 7 + q, 0.35)[:, 0] for q in range(dim)], 1)
+    w = np.array([2.0 * I.uniform01(1999, j) - 1.0 for j in range(n)])
+    pts, wf = tmp_path / "pts.csv", tmp_path / "w.csv"
+    pts.write_text("".join(",".join("%.17g" % v for v in row) + "\n" for row in x))
+    wf.write_text("".join("%.17g\n" % v for v in w))
+    spec, sigma, m, lev = "imq:c=0.5", 3.14159265358979, 16 if dim == 2 else 64, 3
+    lo = [x[:, k].min() - 1e-9 * max(1.0, np.ptp(x[:, k])) for k in range(dim)]
+    hi = [x[:, k].max() + 1e-9 * max(1.0, np.ptp(x[:, k])) for k in range(dim)]
+    common = ["--kernel", spec, "--points", str(pts), "--weights", str(wf),
+              "--sigma", "%.17g" % sigma, "--m", str(m)]
+    outs = {}
+    for mode in ("direct", "single", "mlfmm"):
+        extra = ["--levels", str(lev)] if mode != "direct" else []
+        if mode == "mlfmm":
+            extra += ["--dump-expansions", str(tmp_path / "exp.csv")]
+        rc, _, err = run_cli(["fmm-matvec", "--mode", mode] + common + extra +
+                             ["--out", str(tmp_path / f"u_{mode}.csv")], tmp_path)
+        assert rc == 0, err
+        outs[mode] = read_values(tmp_path / f"u_{mode}.csv")
+    header = open(tmp_path / "u_mlfmm.csv").read()
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)
+    if oracle.ref_available():
+        rd = oracle.ref_direct(x, w, spec)[0]
+        rs, sst = oracle.ref_single(x, w, spec, sigma, m, lev, lo=lo, hi=hi)
+        rm, mst = oracle.ref_mlfmm(x, w, spec, sigma, m, lev, lo=lo, hi=hi)
+        ex = [oracle.ref_expansions(x, w, spec, sigma, m, lev, l, 0, lo=lo, hi=hi)
+              for l in range(2, lev + 1)]
+    else:
+        rd = oracle.direct(x, w, spec)
+        rs, sst, _ = oracle.mlfmm(x, w, spec, sigma, m, lev, lo=lo, hi=hi)
+        rm, mst, _ = oracle.mlfmm(x, w, spec, sigma, m, lev, lo=lo, hi=hi)
+        ex = None
+    assert rel(outs["direct"], rd) <= 1e-12
+    assert rel(outs["single"], rs) <= 1e-10
+    assert rel(outs["mlfmm"], rm) <= 1e-10
+    assert f"# near_pairs: {mst['near_pairs']}" in header
+    assert f"# far_work: {mst['far_work']}" in header
+    if ex is not None:
+        rows = read_csv(tmp_path / "exp.csv")[1:]
+        got = {}
+        for r in rows:
+            got[(int(r[0]), int(r[1]), int(r[2]))] = float(r[3]) + 1j * float(r[4])
+        for li, l in enumerate(range(2, lev + 1)):
+            ref = ex[li]
+            g = np.array([[got[(l, b, e)] for e in range(ref.shape[1])] for b in range(ref.shape[0])])
+            assert np.linalg.norm(g - ref) <= 1e-10 * max(np.linalg.norm(ref), 1e-300)
