@@ -145,6 +145,9 @@ typedef struct blfmm_tuning {
                            real-weight DMMA GEMMs over all right-hand sides
                            (k_p2m_mr / k_l2p_mr); 0: one right-hand side per
                            CTA (k_p2m_m2m_h16 / k_l2p_h16S); -1: default (1) */
+  int half_spectrum;    /* 3-D shared grids, even M in [16, 64]: store the
+                           Hermitian half spectrum (0: the full grid);
+                           -1: default (1) */
 } blfmm_tuning;
 
 /* Per-stage device times of the last execute (CUDA events on the launch

@@ -61,7 +61,8 @@ class Tuning(ct.Structure):
     """blfmm_tuning (include/blfmm_gpu.h): kernel / schedule selection."""
     _fields_ = [("telescope", ct.c_int), ("graphs", ct.c_int), ("near_sym_min", ct.c_int),
                 ("near_ctas_per_sm", ct.c_int), ("near_reg_cap", ct.c_int),
-                ("couple_tile", ct.c_int), ("rhs_gemm", ct.c_int)]
+                ("couple_tile", ct.c_int), ("rhs_gemm", ct.c_int),
+                ("half_spectrum", ct.c_int)]
 
 
 # blfmm_comm_ops callbacks: (ctx, device pointer, count, [root,] stream) -> 0 / error

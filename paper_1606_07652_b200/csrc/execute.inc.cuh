@@ -133,7 +133,7 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
   // P2M (exchange mode: the owned leaves and their halo only)
   // P2M fused with the leaf-level M2M (whole-matvec phase, half spectrum)
   const bool fuse_up =
-      phase == 0 && p->herm && !p->mr && p->n_p2m_plist > 0 && !p->scaled && !p->xbuf;
+      phase == 0 && p->h16 && !p->mr && p->n_p2m_plist > 0 && !p->scaled && !p->xbuf;
   const int* leaf_list = phase == 1 ? p->eleaf.as<int>() : nullptr;
   const long long np2m = phase == 1 ? p->n_eleaf : leaf.nbox;
   if (up && np2m) {
@@ -180,7 +180,30 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
       // read-back; 8 warps, 1 CTA per SM), else 64-point spans (3 CTAs / SM)
       if (p->max_leaf_pts > 64 && p->p2m_span != 64) launch_mr(k_p2m_mr<128, 8>, 128, 8);
       else launch_mr(k_p2m_mr<64, 4>, 64, 4);
-    } else if (D == 3 && p->herm) {
+    } else if (D == 3 && p->herm && !p->h16) {
+      // half spectrum, even M != 16: block A on the large-M kernel (upper m3
+      // half), blocks C / B1 / B2 as three small GEMMs
+      const int H = M / 2;
+      const long long rtiles = ((long long)M * M + 7) / 8;
+      const int smem = (int)(sizeof(double2) * kBigPts * H);
+      dim3 grid((unsigned)np2m, (unsigned)((rtiles + 7) / 8), R);
+      auto lb = [&](auto kern) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        kern<<<grid, 256, smem, st>>>(leaf_list, p->leaf_start.as<int>(), p->pht.as<double2>(),
+                                      p->lam.as<double>(), M, K, n, leaf.nbox,
+                                      leaf.mult.as<double2>(), H, H);
+      };
+      if (H <= 32) lb(k_p2m_big<4>);
+      else lb(k_p2m_big<8>);
+      const int smx = (int)(sizeof(double2) * kBigPts * 64);
+      CK(cudaFuncSetAttribute(k_p2m_axes, cudaFuncAttributeMaxDynamicSharedMemorySize, smx));
+      k_p2m_axes<<<dim3((unsigned)np2m, 3, R), 256, smx, st>>>(
+          leaf_list, p->leaf_start.as<int>(), p->pht.as<double2>(), p->lam.as<double>(), M, K, n,
+          leaf.nbox, leaf.mult.as<double2>());
+      if (p->hK < K)  // padding nodes stay zero
+        CK(cudaMemset2DAsync(leaf.mult.as<double2>() + p->hK, sizeof(double2) * K, 0,
+                             sizeof(double2) * (K - p->hK), (size_t)R * leaf.nbox, st));
+    } else if (D == 3 && p->h16) {
       dim3 grid((unsigned)np2m, 1, R);
       k_p2m_h16w4<<<grid, 128, 0, st>>>(leaf_list, p->leaf_start.as<int>(), p->pht.as<double2>(),
                                         p->lam.as<double>(), n, leaf.nbox, leaf.mult.as<double2>());
@@ -192,7 +215,7 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         kern<<<grid, 256, smem, st>>>(leaf_list, p->leaf_start.as<int>(), p->pht.as<double2>(),
                                       p->lam.as<double>(), M, K, n, leaf.nbox,
-                                      leaf.mult.as<double2>());
+                                      leaf.mult.as<double2>(), 0, M);
       };
       if (M <= 32) lb(k_p2m_big<4>);
       else lb(k_p2m_big<8>);
@@ -504,7 +527,18 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
                                     p->node_m.as<int>(), p->dtab.as<double>(),
                                     leaf.loc.as<double2>(), R, n, leaf.nbox, p->weight,
                                     p->far_.as<double>(), p->imag_bits.as<unsigned long long>());
-    } else if (D == 3 && p->herm) {
+    } else if (D == 3 && p->herm && !p->h16) {
+      dim3 gr((unsigned)p->nwork8, 1, R);
+      k_l2p_axes<<<gr, 128, 0, st>>>(p->work8.as<int2>(), p->leaf_start.as<int>(),
+                                     p->pht.as<double2>(), leaf.loc.as<double2>(), M, K, n,
+                                     leaf.nbox, p->weight, p->far_.as<double>(),
+                                     p->himag.as<double>());
+      auto la = p->want_imag ? k_l2p_half_a<4, true> : k_l2p_half_a<4, false>;
+      la<<<gr, 128, 0, st>>>(p->work8.as<int2>(), p->leaf_start.as<int>(), p->pht.as<double2>(),
+                             leaf.loc.as<double2>(), p->dtab.as<double>(), M, K, n, leaf.nbox,
+                             p->weight, p->far_.as<double>(), p->himag.as<double>(),
+                             p->imag_bits.as<unsigned long long>());
+    } else if (D == 3 && p->h16) {
       dim3 grid((unsigned)p->nwork128, 1, R);
       // the D-weighted GEMM of max|Im| only when the caller asked for stats
       auto l2pS = p->want_imag ? k_l2p_h16S<4, true> : k_l2p_h16S<4, false>;

@@ -592,9 +592,12 @@ template <int MCT>
 __global__ void __launch_bounds__(256, 1)
     k_p2m_big(const int* __restrict__ leaf_list, const int* __restrict__ leaf_start,
               const double2* __restrict__ pht, const double* __restrict__ lam, int M,
-              long long K, long long n, long long nleaf, double2* __restrict__ mult) {
+              long long K, long long n, long long nleaf, double2* __restrict__ mult,
+              int coff, int ncol) {
+  // columns m3 = coff .. coff + ncol - 1, stored at row * ncol + (m3 - coff):
+  // the full grid (0, M), or block A of the half spectrum (M / 2, M / 2)
   extern __shared__ __align__(16) double2 big_dyn[];
-  double2* s3 = big_dyn;                                   // [kBigPts][M]  lambda conj(P3)
+  double2* s3 = big_dyn;                                   // [kBigPts][ncol]  lambda conj(P3)
   const long long a = leaf_list ? leaf_list[blockIdx.x] : blockIdx.x;
   const int r = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -612,11 +615,11 @@ __global__ void __launch_bounds__(256, 1)
   for (int c0 = p0; c0 < p1; c0 += kBigPts) {
     const int nb = min(kBigPts, p1 - c0);
     __syncthreads();
-    for (int t = threadIdx.x; t < nb * M; t += blockDim.x) {
-      const int j = t / M, c = t % M;
-      const double2 z = __ldg(pht + (long long)(c0 + j) * per + 2 * M + c);
+    for (int t = threadIdx.x; t < nb * ncol; t += blockDim.x) {
+      const int j = t / ncol, c = t % ncol;
+      const double2 z = __ldg(pht + (long long)(c0 + j) * per + 2 * M + coff + c);
       const double w = __ldg(lr + c0 + j);
-      s3[j * M + c] = make_double2(w * z.x, -w * z.y);
+      s3[j * ncol + c] = make_double2(w * z.x, -w * z.y);
     }
     __syncthreads();
     for (int j0 = 0; j0 < nb; j0 += 4) {
@@ -631,7 +634,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int u = 0; u < MCT; ++u) {
         const int col = 8 * u + g;
-        const double2 b = (jv && col < M) ? s3[j * M + col] : make_double2(0.0, 0.0);
+        const double2 b = (jv && col < ncol) ? s3[j * ncol + col] : make_double2(0.0, 0.0);
         cdmma(acc[u], are, aim, -aim, b.x, b.y);
       }
     }
@@ -644,7 +647,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       const int col = 8 * u + 2 * tq + v;
-      if (col < M) out[orow * M + col] = make_double2(acc[u].re[v], acc[u].im[v]);
+      if (col < ncol) out[orow * ncol + col] = make_double2(acc[u].re[v], acc[u].im[v]);
     }
   }
 }

@@ -1,0 +1,247 @@
+// Hermitian half spectrum for any even M (3-D, shared grids; M = 16 has its
+// own fused kernels in k_half_dmma.inc.cuh). Stored nodes per box, H = M / 2:
+//   A   rows (m1, m2) x m3 in [H, M)             e = (m1 M + m2) H + m3 - H
+//   C   the m3 = 0 plane                          e = oC + m1 M + m2
+//   B1  m1 = 0, m2 in [0, M), m3 in [1, H)       e = oB + m2 (H - 1) + m3 - 1
+//   B2  m2 = 0, m1 in [1, M), m3 in [1, H)       e = oB + (M - 1 + m1)(H - 1) + m3 - 1
+// (oC = M^2 H, oB = oC + M^2; the M = 16 layout of build_h16 is this one).
+// The missing nodes are the mirrors (M - m1, M - m2, M - m3) of the block-A
+// nodes with m1, m2 >= 1, m3 >= H + 1, whose C weights fold into Ct (see
+// build_half). P2M / L2P of block A are the large-M DMMA GEMMs restricted to
+// the upper m3 half (k_p2m_big with a column window, k_l2p_half_a); blocks C,
+// B1, B2 are three small two-axis GEMMs per leaf / point tile (k_p2m_axes,
+// k_l2p_axes) with the third axis folded into the per-point weight.
+// Fragment of blfmm.cu (one translation unit): included inside namespace
+// blfmm_gpu; not a standalone header.
+
+struct HalfAxes {  // one of the blocks C / B1 / B2
+  int ax, a0, na;  // row axis, first index, count
+  int bx, b0, nb;  // column axis
+  int fx, f0;      // fixed axis folded into the point weight
+  long long off;   // element offset of the block inside the box
+  int stride;      // row stride of the block
+};
+__device__ __forceinline__ HalfAxes half_block(int blk, int M) {
+  const int H = M / 2;
+  const long long oC = (long long)M * M * H, oB = oC + (long long)M * M;
+  if (blk == 0) return HalfAxes{0, 0, M, 1, 0, M, 2, 0, oC, M};
+  if (blk == 1) return HalfAxes{1, 0, M, 2, 1, H - 1, 0, 0, oB, H - 1};
+  return HalfAxes{0, 1, M - 1, 2, 1, H - 1, 1, 0, oB + (long long)M * (H - 1), H - 1};
+}
+
+// P2M of blocks C / B1 / B2 (blockIdx.y): V[a][b] = sum_j conj(Pa_j[a])
+// (lambda_j conj(Pf_j[f0]) conj(Pb_j[b])); 8 warps = 8 row tiles, all column
+// tiles per warp, the B operand of a 64-point chunk staged in shared memory.
+__global__ void __launch_bounds__(256, 1)
+    k_p2m_axes(const int* __restrict__ leaf_list, const int* __restrict__ leaf_start,
+               const double2* __restrict__ pht, const double* __restrict__ lam, int M,
+               long long K, long long n, long long nleaf, double2* __restrict__ mult) {
+  extern __shared__ __align__(16) double2 ax_dyn[];  // [kBigPts][64]
+  const HalfAxes hb = half_block(blockIdx.y, M);
+  const long long lf = leaf_list ? leaf_list[blockIdx.x] : blockIdx.x;
+  const int r = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int ra = 8 * warp + g;  // this lane's A row (block row a0 + ra)
+  const bool rv = ra < hb.na;
+  const int p0 = leaf_start[lf], p1 = leaf_start[lf + 1];
+  const double* lr = lam + (long long)r * n;
+  const int per = 3 * M;
+  CTile acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = CTile{{0.0, 0.0}, {0.0, 0.0}};
+  for (int c0 = p0; c0 < p1; c0 += kBigPts) {
+    const int np = min(kBigPts, p1 - c0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < np * hb.nb; t += blockDim.x) {
+      const int j = t / hb.nb, c = t % hb.nb;
+      const double2* pj = pht + (long long)(c0 + j) * per;
+      const double w = __ldg(lr + c0 + j);
+      const double2 z = cmul(__ldg(pj + hb.fx * M + hb.f0), __ldg(pj + hb.bx * M + hb.b0 + c));
+      ax_dyn[j * 64 + c] = make_double2(w * z.x, -w * z.y);  // lambda conj(Pf Pb)
+    }
+    __syncthreads();
+    for (int j0 = 0; j0 < np; j0 += 4) {
+      const int j = j0 + tq;
+      const bool jv = j < np;
+      double2 za = make_double2(0.0, 0.0);
+      if (jv && rv) za = __ldg(pht + (long long)(c0 + j) * per + hb.ax * M + hb.a0 + ra);
+      const double are = za.x, aim = -za.y;  // conj(Pa)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int col = 8 * u + g;
+        const double2 b = (jv && col < hb.nb) ? ax_dyn[j * 64 + col] : make_double2(0.0, 0.0);
+        cdmma(acc[u], are, aim, -aim, b.x, b.y);
+      }
+    }
+  }
+  if (!rv) return;
+  double2* out = mult + ((long long)r * nleaf + lf) * K + hb.off + (long long)ra * hb.stride;
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int col = 8 * u + 2 * tq + v;
+      if (col < hb.nb) out[col] = make_double2(acc[u].re[v], acc[u].im[v]);
+    }
+}
+
+// L2P of blocks C / B1 / B2 for an 8-point tile (work8): for each block
+// W_i[a] = sum_b Pb_i[b] L[a][b] on DMMA (A = the points' Pb, B = L^T; warp w
+// takes row tiles w and w + 4), then part_i += Pf_i[f0] sum_a Pa_i[a] W_i[a].
+// Writes far_[i] = w Re part_i and imag_acc[i] = w Im part_i (block A adds to
+// both afterwards, k_l2p_half_a).
+__global__ void __launch_bounds__(128)
+    k_l2p_axes(const int2* __restrict__ work, const int* __restrict__ leaf_start,
+               const double2* __restrict__ pht, const double2* __restrict__ loc, int M,
+               long long K, long long n, long long nleaf, double weight,
+               double* __restrict__ far_, double* __restrict__ imag_acc) {
+  __shared__ double2 red[4][8];
+  const int2 item = work[blockIdx.x];
+  const long long lf = item.x;
+  const int r = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int p1 = leaf_start[lf + 1], pb = item.y;
+  const int per = 3 * M;
+  const int ia = pb + g;  // A row / C row: point
+  const bool iv = ia < p1;
+  const double2* pi = pht + (long long)(iv ? ia : pb) * per;
+  const double2* la = loc + ((long long)r * nleaf + lf) * K;
+  double2 part = make_double2(0.0, 0.0);
+  for (int blk = 0; blk < 3; ++blk) {
+    const HalfAxes hb = half_block(blk, M);
+    const double2 pf = __ldg(pi + hb.fx * M + hb.f0);
+    double2 bpart = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int rt = warp + 4 * q;  // row tile of a
+      if (8 * rt >= hb.na) continue;
+      const int arow = 8 * rt + g;  // B column n = g: row a of L
+      const bool av = arow < hb.na;
+      CTile acc = CTile{{0.0, 0.0}, {0.0, 0.0}};
+      for (int k0 = 0; k0 < hb.nb; k0 += 4) {
+        const int c = k0 + tq;
+        const bool cv = c < hb.nb;
+        const double2 z = (iv && cv) ? __ldg(pi + hb.bx * M + hb.b0 + c) : make_double2(0.0, 0.0);
+        const double2 lv = (av && cv) ? __ldg(la + hb.off + (long long)arow * hb.stride + c)
+                                      : make_double2(0.0, 0.0);
+        cdmma(acc, z.x, z.y, -z.y, lv.x, lv.y);
+      }
+      // C[point g][a = 8 rt + 2 tq + v]
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int aa = 8 * rt + 2 * tq + v;
+        if (aa >= hb.na || !iv) continue;
+        cmac(bpart, __ldg(pi + hb.ax * M + hb.a0 + aa), make_double2(acc.re[v], acc.im[v]));
+      }
+    }
+    cmac(part, pf, bpart);
+  }
+  for (int off = 1; off < 4; off <<= 1) {
+    part.x += __shfl_xor_sync(0xffffffffu, part.x, off);
+    part.y += __shfl_xor_sync(0xffffffffu, part.y, off);
+  }
+  if (tq == 0) red[warp][g] = part;
+  __syncthreads();
+  if (threadIdx.x < 8 && pb + threadIdx.x < p1) {
+    double2 sum = red[0][threadIdx.x];
+    for (int w = 1; w < 4; ++w) {
+      sum.x += red[w][threadIdx.x].x;
+      sum.y += red[w][threadIdx.x].y;
+    }
+    far_[(long long)r * n + pb + threadIdx.x] = weight * sum.x;
+    imag_acc[(long long)r * n + pb + threadIdx.x] = weight * sum.y;
+  }
+}
+
+// L2P of block A for an 8-point tile: W_i[row] = sum_{m3 >= H} P3_i[m3]
+// L[row][m3 - H] on DMMA (k_l2p_mma's tiling, K = H), then u_i += w Re sum_row
+// P1_i[m1] P2_i[m2] W_i[row]; IM: the imaginary residual of a mirrored pair is
+// (C_m - C_m') Im T, so the imaginary part uses the locals scaled by D
+// (dtab), added to the blocks' imag_acc and max-reduced.
+template <int WN, bool IM>
+__global__ void __launch_bounds__(128)
+    k_l2p_half_a(const int2* __restrict__ work, const int* __restrict__ leaf_start,
+                 const double2* __restrict__ pht, const double2* __restrict__ loc,
+                 const double* __restrict__ dtab, int M, long long K, long long n,
+                 long long nleaf, double weight, double* __restrict__ far_,
+                 const double* __restrict__ imag_acc, unsigned long long* __restrict__ imag_bits) {
+  __shared__ double2 red[4][8];
+  const int2 item = work[blockIdx.x];
+  const long long lf = item.x;
+  const int r = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int H = M / 2;
+  const long long rows = (long long)M * M, rtiles = (rows + 7) / 8;
+  const int p1 = leaf_start[lf + 1], pb = item.y;
+  const int per = 3 * M;
+  const int ia = pb + g;
+  const bool iv = ia < p1;
+  const double2* pa = pht + (long long)(iv ? ia : pb) * per;
+  const double2* la = loc + ((long long)r * nleaf + lf) * K;
+  double2 part = make_double2(0.0, 0.0);
+  double pim = 0.0;
+  for (long long tb = (long long)warp * WN; tb < rtiles; tb += 4LL * WN) {
+    CTile acc[WN], acd[WN];
+#pragma unroll
+    for (int u = 0; u < WN; ++u) acc[u] = acd[u] = CTile{{0.0, 0.0}, {0.0, 0.0}};
+    const double2* lrow[WN];
+    bool bv[WN];
+#pragma unroll
+    for (int u = 0; u < WN; ++u) {
+      const long long row = (tb + u) * 8 + g;
+      bv[u] = (tb + u) < rtiles && row < rows;
+      lrow[u] = la + (bv[u] ? row : 0) * H;
+    }
+    for (int k0 = 0; k0 < H; k0 += 4) {
+      const int c = k0 + tq;
+      const bool kv = c < H;
+      const double2 z = (iv && kv) ? __ldg(pa + 2 * M + H + c) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < WN; ++u) {
+        const double2 lv = (bv[u] && kv) ? __ldg(lrow[u] + c) : make_double2(0.0, 0.0);
+        cdmma(acc[u], z.x, z.y, -z.y, lv.x, lv.y);
+        if (IM) {
+          const long long row = (tb + u) * 8 + g;
+          const double dv = (bv[u] && kv) ? __ldg(dtab + row * H + c) : 0.0;
+          cdmma(acd[u], z.x, z.y, -z.y, dv * lv.x, dv * lv.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < WN; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const long long row = (tb + u) * 8 + 2 * tq + v;
+        if ((tb + u) >= rtiles || row >= rows || !iv) continue;
+        const double2 p12 = cmul(__ldg(pa + row / M), __ldg(pa + M + row % M));
+        cmac(part, p12, make_double2(acc[u].re[v], acc[u].im[v]));
+        if (IM) {
+          const double2 wd = make_double2(acd[u].re[v], acd[u].im[v]);
+          pim += p12.x * wd.y + p12.y * wd.x;
+        }
+      }
+  }
+  for (int off = 1; off < 4; off <<= 1) {
+    part.x += __shfl_xor_sync(0xffffffffu, part.x, off);
+    pim += __shfl_xor_sync(0xffffffffu, pim, off);
+  }
+  if (tq == 0) red[warp][g] = make_double2(part.x, pim);
+  __syncthreads();
+  if (threadIdx.x < 8 && pb + threadIdx.x < p1) {
+    double2 sum = red[0][threadIdx.x];
+    for (int w = 1; w < 4; ++w) {
+      sum.x += red[w][threadIdx.x].x;
+      sum.y += red[w][threadIdx.x].y;
+    }
+    const long long i = (long long)r * n + pb + threadIdx.x;
+    far_[i] += weight * sum.x;
+    if (IM) {
+      const double im = fabs(imag_acc[i] + weight * sum.y);
+      if (im > 0.0)
+        atomicMax(imag_bits, static_cast<unsigned long long>(__double_as_longlong(im)));
+    }
+  }
+}

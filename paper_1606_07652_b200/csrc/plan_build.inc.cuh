@@ -64,33 +64,43 @@ void cub_call(DevBuf& scratch, cudaStream_t st, F&& f) {
 
 // Per-level phase tables (host, double): m2m[l][k][delta][m] =
 // e^{i xi_m (1/2 - delta) h_{l,k}}, m2l[l][k][o+3][m] = e^{-i xi_m o h_{l,k}}.
-// Hermitian half-spectrum node table and Ct (see the block comment above k_p2m_h16w4).
-void build_h16(const std::vector<double>& c, std::vector<int>& node, std::vector<double>& ct,
-               std::vector<double>& dt) {
-  node.assign(kH16Ks, 0);
-  ct.assign(kH16Ks, 0.0);
-  dt.assign(kH16Ks, 0.0);
-  auto full = [](int m1, int m2, int m3) { return (m1 * 16 + m2) * 16 + m3; };
-  auto put = [&](int e, int m1, int m2, int m3) {
+// Hermitian half-spectrum node table, Ct and D for an even M (layout in
+// k_halfm.inc.cuh; M = 16 is the layout the k_*_h16* kernels tile): node[e] =
+// m1 | m2 << 8 | m3 << 16; Ct = C_m + C_m' and D = (C_m - C_m') / Ct for the
+// block-A nodes whose mirror m' = (M - m1, M - m2, M - m3) is not stored
+// (m1, m2 >= 1, m3 >= M/2 + 1), Ct = C_m and D = 1 otherwise. Returns the
+// stored count; the vectors are padded to a multiple of 32 nodes.
+long long build_half(const std::vector<double>& c, int M, std::vector<int>& node,
+                     std::vector<double>& ct, std::vector<double>& dt) {
+  const int H = M / 2;
+  const long long nA = (long long)M * M * H, nC = (long long)M * M,
+                  nB = (long long)(2 * M - 1) * (H - 1);
+  const long long K = nA + nC + nB, Ks = (K + 31) / 32 * 32;
+  node.assign(Ks, 0);
+  ct.assign(Ks, 0.0);
+  dt.assign(Ks, 0.0);
+  auto full = [M](int m1, int m2, int m3) { return ((long long)m1 * M + m2) * M + m3; };
+  auto put = [&](long long e, int m1, int m2, int m3) {
     node[e] = m1 | (m2 << 8) | (m3 << 16);
     const double v = c[full(m1, m2, m3)];
     ct[e] = v;
     dt[e] = 1.0;
-    if (m1 >= 1 && m2 >= 1 && m3 >= 9) {
-      const double vm = c[full(16 - m1, 16 - m2, 16 - m3)];
+    if (m1 >= 1 && m2 >= 1 && m3 >= H + 1) {
+      const double vm = c[full(M - m1, M - m2, M - m3)];
       ct[e] = v + vm;
       dt[e] = ct[e] != 0.0 ? (v - vm) / ct[e] : 0.0;
     }
   };
-  for (int row = 0; row < 256; ++row)
-    for (int m3 = 8; m3 < 16; ++m3) put(row * 8 + m3 - 8, row / 16, row % 16, m3);
-  for (int m1 = 0; m1 < 16; ++m1)
-    for (int m2 = 0; m2 < 16; ++m2) put(kH16A + m1 * 16 + m2, m1, m2, 0);
-  for (int rb = 0; rb < kH16BR; ++rb) {
-    int m1, m2;
-    h16_brow(rb, m1, m2);
-    for (int m3 = 1; m3 < 8; ++m3) put(kH16A + kH16C + rb * 7 + m3 - 1, m1, m2, m3);
+  for (int m1 = 0; m1 < M; ++m1)
+    for (int m2 = 0; m2 < M; ++m2)
+      for (int m3 = H; m3 < M; ++m3) put(((long long)m1 * M + m2) * H + m3 - H, m1, m2, m3);
+  for (int m1 = 0; m1 < M; ++m1)
+    for (int m2 = 0; m2 < M; ++m2) put(nA + (long long)m1 * M + m2, m1, m2, 0);
+  for (int rb = 0; rb < 2 * M - 1; ++rb) {
+    const int m1 = rb < M ? 0 : rb - M + 1, m2 = rb < M ? rb : 0;
+    for (int m3 = 1; m3 < H; ++m3) put(nA + nC + (long long)rb * (H - 1) + m3 - 1, m1, m2, m3);
   }
+  return K;
 }
 
 // Segment tables of the z-streamed leaf couple (k_couple_col): the leaf
@@ -799,12 +809,16 @@ void create_plan(const blfmm_plan_desc* desc, const blfmm_tuning* tune, blfmm_pl
                       : translation_spectrum(k, p->sigma, p->M, d);
   }
   p->Ks = K;
-  p->herm = d == 3 && p->M == 16 && !p->scaled;
-  p->mr = p->herm && p->R >= 8 && !(tune && tune->rhs_gemm == 0);
+  // half spectrum: 3-D shared grids, even M in [16, 64] (M = 16: the tiled
+  // k_*_h16* kernels; otherwise block GEMMs, k_halfm.inc.cuh)
+  p->herm = d == 3 && !p->scaled && p->M % 2 == 0 && p->M >= 16 && p->M <= 64 &&
+            !(tune && tune->half_spectrum == 0);
+  p->h16 = p->herm && p->M == 16;
+  p->mr = p->h16 && p->R >= 8 && !(tune && tune->rhs_gemm == 0);
   if (p->herm) {
     std::vector<double> dt;
-    build_h16(c, p->node_host, p->c_st, dt);
-    p->Ks = kH16Ks;
+    p->hK = build_half(c, p->M, p->node_host, p->c_st, dt);
+    p->Ks = static_cast<long long>(p->node_host.size());
     upload(p->node_m, p->node_host);
     upload(p->dtab, dt);
     upload(p->ctab, p->c_st);
@@ -864,6 +878,7 @@ void create_plan(const blfmm_plan_desc* desc, const blfmm_tuning* tune, blfmm_pl
     CK(cudaStreamSynchronize(p->stream));
   }
   p->imag_bits.alloc(sizeof(unsigned long long));
+  if (p->herm && !p->h16) p->himag.alloc(sizeof(double) * R * std::max<long long>(n, 1));
   if (d == 3 && !p->scaled) p->root.alloc(sizeof(double2) * R * Ks);
 
   // multi-GPU exchange mode: halo sets and exchange-buffer layout
@@ -937,8 +952,9 @@ void create_plan(const blfmm_plan_desc* desc, const blfmm_tuning* tune, blfmm_pl
     std::string k = "p2m=";
     if (d == 1) k += "k_p2m";
     else if (p->mr) k += "k_p2m_mr";
-    else if (p->herm && p->n_p2m_plist > 0) k += "k_p2m_m2m_h16";
-    else if (p->herm) k += "k_p2m_h16w4";
+    else if (p->h16 && p->n_p2m_plist > 0) k += "k_p2m_m2m_h16";
+    else if (p->h16) k += "k_p2m_h16w4";
+    else if (p->herm) k += "k_p2m_big(half)+k_p2m_axes";
     else if (p->g2d16) k += "k_p2m_2d16";
     else if (d == 3 && p->M >= 24 && p->M <= 64 && !p->scaled) k += "k_p2m_big";
     else k += "k_p2m_mma";
@@ -951,7 +967,8 @@ void create_plan(const blfmm_plan_desc* desc, const blfmm_tuning* tune, blfmm_pl
     else k += d == 3 ? " couple=k_couple3" : " couple=k_couple";
     k += d == 1 ? " l2p=k_l2p"
                 : (p->mr ? " l2p=k_l2p_mr"
-                         : (p->herm ? " l2p=k_l2p_h16S"
+                         : (p->h16 ? " l2p=k_l2p_h16S"
+                                   : p->herm ? " l2p=k_l2p_axes+k_l2p_half_a"
                                     : (p->g2d16 ? " l2p=k_l2p_2d16" : " l2p=k_l2p_mma")));
     if (p->R == 1)
       k += " near=k_near_all(ctas_per_sm=" + std::to_string(p->near_persist) +

@@ -682,3 +682,46 @@ def test_rhs_gemm_matches_per_rhs_path_and_oracle(blfmm, oracle, name, n, leaf, 
     ctab = blfmm.translation_coefficients(k, blfmm.make_quadrature(W.sigma, W.m, 3)).c_vals
     ov, _, _ = oracle.mlfmm(x, w[[0, nr - 1]], W.kernel, W.sigma, W.m, leaf, c_table_in=ctab)
     assert rel_l2(rg.values[0], ov[0]) <= TOL and rel_l2(rg.values[nr - 1], ov[1]) <= TOL
+
+
+@pytest.mark.parametrize("spec,m,n,leaf", [("imq:c=0.1", 20, 6000, 3), ("gaussian:c=64", 32, 8000, 3),
+                                           ("mq:c=0.2", 58, 4096, 2), ("imq:c=0.1", 34, 30000, 4)])
+def test_half_spectrum_general_even_m(blfmm, oracle, spec, m, n, leaf):
+    """Hermitian half spectrum for even M != 16 (block A on the large-M DMMA
+    kernels restricted to the upper m3 half, blocks C / B1 / B2 as small
+    GEMMs, k_halfm.inc.cuh): equal to the full-grid plan (tuning
+    half_spectrum = 0) to rounding, to the oracle at the north-star bar,
+    max|Im| (the D-weighted imaginary residual) equal, and the stage
+    expansions rebuilt on the full grid."""
+    W = I.WORKLOADS["P3"]
+    x, w = W.make(n)
+    sigma = math.pi
+    rh, ph = gpu_mlfmm(blfmm, x, w, spec, sigma, m, leaf)
+    rf, pf = gpu_mlfmm(blfmm, x, w, spec, sigma, m, leaf, tuning={"half_spectrum": 0})
+    assert ph.info().stored_nodes < pf.info().stored_nodes == m ** 3
+    assert "k_p2m_axes" in ph.kernels()["p2m"] and "k_l2p_half_a" in ph.kernels()["l2p"]
+    assert rel_l2(rh.values, rf.values) <= 1e-13, rel_l2(rh.values, rf.values)
+    assert abs(rh.stats.max_imag_residual - rf.stats.max_imag_residual) <= \
+        1e-9 * max(1.0, rf.stats.max_imag_residual)
+    assert rh.stats.near_pairs == rf.stats.near_pairs and rh.stats.far_work == rf.stats.far_work
+    ctab = blfmm.translation_coefficients(blfmm.parse_kernel_spec(spec),
+                                          blfmm.make_quadrature(sigma, m, 3)).c_vals
+    ov, ost, _ = oracle.mlfmm(x, w, spec, sigma, m, leaf, c_table_in=ctab)
+    assert rel_l2(rh.values, ov) <= TOL
+    assert abs(rh.stats.max_imag_residual - ost["max_imag_residual"]) <= \
+        1e-8 * max(1.0, ost["max_imag_residual"])
+    if n <= 8000:  # upsweep multipoles of the leaf level, full grid, reference box order
+        eh = ph.expansions(leaf, 0)
+        ef = pf.expansions(leaf, 0)
+        assert np.linalg.norm(eh - ef) <= 1e-12 * np.linalg.norm(ef)
+
+
+def test_half_spectrum_general_even_m_batched(blfmm, oracle):
+    """The general half spectrum with several right-hand sides (grid.z = R)."""
+    W = I.WORKLOADS["P5"]
+    x, w = W.make(6000)
+    w = np.ascontiguousarray(w[:3])
+    rh, ph = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, 24, 3)
+    rf, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, 24, 3, tuning={"half_spectrum": 0})
+    assert "k_p2m_axes" in ph.kernels()["p2m"]
+    assert rel_l2(rh.values, rf.values) <= 1e-13

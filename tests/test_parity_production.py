@@ -112,13 +112,15 @@ def test_p3_mid_size_symmetric_near_field_matches_oracle(blfmm, oracle):
 
 def test_p2_full_size_matches_oracle_on_target_subset(blfmm, oracle):
     """BASELINE configs[1]: 3-D Gaussian eps=8 (c=64), N=262,144, sigma=101.8,
-    M=58 (K=195,112), leaf 4 - full-grid DMMA P2M / L2P (k_p2m_big / k_l2p_mma) and the telescoped
+    M=58 (K=195,112; 104,160 stored: the Hermitian half spectrum), leaf 4 - the block-A
+    DMMA GEMMs and the C / B1 / B2 block GEMMs of P2M / L2P and the telescoped
     couple at K=195k - against the oracle on 24 seeded target leaves."""
     W = I.WORKLOADS["P2"]
     x, w = W.make()
     plan = production_plan(blfmm, W, x)
     k = plan.kernels()
-    assert k["p2m"] == "k_p2m_big" and k["l2p"] == "k_l2p_mma", k
+    assert k["p2m"] == "k_p2m_big(half)+k_p2m_axes" and k["l2p"] == "k_l2p_axes+k_l2p_half_a", k
+    assert plan.info().stored_nodes < 58 ** 3  # Hermitian half spectrum
     assert k["couple"] == "k_root+k_couple_col<2x2,z32>", k
     assert k["near"].startswith("k_near_all(") and plan.info().near_sym_items > 0, k
     res = plan.execute(w)
