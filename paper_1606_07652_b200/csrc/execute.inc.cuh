@@ -533,11 +533,15 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
                                      p->pht.as<double2>(), leaf.loc.as<double2>(), M, K, n,
                                      leaf.nbox, p->weight, p->far_.as<double>(),
                                      p->himag.as<double>());
-      auto la = p->want_imag ? k_l2p_half_a<4, true> : k_l2p_half_a<4, false>;
-      la<<<gr, 128, 0, st>>>(p->work8.as<int2>(), p->leaf_start.as<int>(), p->pht.as<double2>(),
-                             leaf.loc.as<double2>(), p->dtab.as<double>(), M, K, n, leaf.nbox,
-                             p->weight, p->far_.as<double>(), p->himag.as<double>(),
-                             p->imag_bits.as<unsigned long long>());
+      // block A: 32 points per CTA (16 with the imaginary-residual GEMM)
+      auto la = [&](auto kern, const DevBuf& wk, long long nw) {
+        kern<<<dim3((unsigned)nw, 1, R), 128, 0, st>>>(
+            wk.as<int2>(), p->leaf_start.as<int>(), p->pht.as<double2>(), leaf.loc.as<double2>(),
+            p->dtab.as<double>(), M, K, n, leaf.nbox, p->weight, p->far_.as<double>(),
+            p->himag.as<double>(), p->imag_bits.as<unsigned long long>());
+      };
+      if (p->want_imag) la(k_l2p_half_a<2, 1, true>, p->work8, p->nwork8);
+      else la(k_l2p_half_a<2, 4, false>, p->work32, p->nwork32);
     } else if (D == 3 && p->h16) {
       dim3 grid((unsigned)p->nwork128, 1, R);
       // the D-weighted GEMM of max|Im| only when the caller asked for stats

@@ -160,14 +160,16 @@ __global__ void __launch_bounds__(128)
 // P1_i[m1] P2_i[m2] W_i[row]; IM: the imaginary residual of a mirrored pair is
 // (C_m - C_m') Im T, so the imaginary part uses the locals scaled by D
 // (dtab), added to the blocks' imag_acc and max-reduced.
-template <int WN, bool IM>
+template <int WN, int PT, bool IM>
 __global__ void __launch_bounds__(128)
     k_l2p_half_a(const int2* __restrict__ work, const int* __restrict__ leaf_start,
                  const double2* __restrict__ pht, const double2* __restrict__ loc,
                  const double* __restrict__ dtab, int M, long long K, long long n,
                  long long nleaf, double weight, double* __restrict__ far_,
                  const double* __restrict__ imag_acc, unsigned long long* __restrict__ imag_bits) {
-  __shared__ double2 red[4][8];
+  // PT point tiles (8 PT points of one leaf) per CTA: every block-A local is
+  // read once per 8 PT points instead of once per 8
+  __shared__ double2 red[4][8 * PT];
   const int2 item = work[blockIdx.x];
   const long long lf = item.x;
   const int r = blockIdx.z;
@@ -175,18 +177,26 @@ __global__ void __launch_bounds__(128)
   const int g = lane >> 2, tq = lane & 3;
   const int H = M / 2;
   const long long rows = (long long)M * M, rtiles = (rows + 7) / 8;
-  const int p1 = leaf_start[lf + 1], pb = item.y;
+  const int p1 = min(leaf_start[lf + 1], item.y + 8 * PT), pb = item.y;
   const int per = 3 * M;
-  const int ia = pb + g;
-  const bool iv = ia < p1;
-  const double2* pa = pht + (long long)(iv ? ia : pb) * per;
-  const double2* la = loc + ((long long)r * nleaf + lf) * K;
-  double2 part = make_double2(0.0, 0.0);
-  double pim = 0.0;
-  for (long long tb = (long long)warp * WN; tb < rtiles; tb += 4LL * WN) {
-    CTile acc[WN], acd[WN];
+  const double2* pa[PT];
+  bool iv[PT];
 #pragma unroll
-    for (int u = 0; u < WN; ++u) acc[u] = acd[u] = CTile{{0.0, 0.0}, {0.0, 0.0}};
+  for (int pt = 0; pt < PT; ++pt) {
+    const int ia = pb + 8 * pt + g;
+    iv[pt] = ia < p1;
+    pa[pt] = pht + (long long)(iv[pt] ? ia : pb) * per;
+  }
+  const double2* la = loc + ((long long)r * nleaf + lf) * K;
+  double part[PT], pim[PT];
+#pragma unroll
+  for (int pt = 0; pt < PT; ++pt) part[pt] = pim[pt] = 0.0;
+  for (long long tb = (long long)warp * WN; tb < rtiles; tb += 4LL * WN) {
+    CTile acc[WN][PT], acd[WN][PT];
+#pragma unroll
+    for (int u = 0; u < WN; ++u)
+#pragma unroll
+      for (int pt = 0; pt < PT; ++pt) acc[u][pt] = acd[u][pt] = CTile{{0.0, 0.0}, {0.0, 0.0}};
     const double2* lrow[WN];
     bool bv[WN];
 #pragma unroll
@@ -198,15 +208,22 @@ __global__ void __launch_bounds__(128)
     for (int k0 = 0; k0 < H; k0 += 4) {
       const int c = k0 + tq;
       const bool kv = c < H;
-      const double2 z = (iv && kv) ? __ldg(pa + 2 * M + H + c) : make_double2(0.0, 0.0);
+      double2 z[PT];
+#pragma unroll
+      for (int pt = 0; pt < PT; ++pt)
+        z[pt] = (iv[pt] && kv) ? __ldg(pa[pt] + 2 * M + H + c) : make_double2(0.0, 0.0);
 #pragma unroll
       for (int u = 0; u < WN; ++u) {
         const double2 lv = (bv[u] && kv) ? __ldg(lrow[u] + c) : make_double2(0.0, 0.0);
-        cdmma(acc[u], z.x, z.y, -z.y, lv.x, lv.y);
+        double dv = 0.0;
         if (IM) {
           const long long row = (tb + u) * 8 + g;
-          const double dv = (bv[u] && kv) ? __ldg(dtab + row * H + c) : 0.0;
-          cdmma(acd[u], z.x, z.y, -z.y, dv * lv.x, dv * lv.y);
+          dv = (bv[u] && kv) ? __ldg(dtab + row * H + c) : 0.0;
+        }
+#pragma unroll
+        for (int pt = 0; pt < PT; ++pt) {
+          cdmma(acc[u][pt], z[pt].x, z[pt].y, -z[pt].y, lv.x, lv.y);
+          if (IM) cdmma(acd[u][pt], z[pt].x, z[pt].y, -z[pt].y, dv * lv.x, dv * lv.y);
         }
       }
     }
@@ -215,22 +232,27 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const long long row = (tb + u) * 8 + 2 * tq + v;
-        if ((tb + u) >= rtiles || row >= rows || !iv) continue;
-        const double2 p12 = cmul(__ldg(pa + row / M), __ldg(pa + M + row % M));
-        cmac(part, p12, make_double2(acc[u].re[v], acc[u].im[v]));
-        if (IM) {
-          const double2 wd = make_double2(acd[u].re[v], acd[u].im[v]);
-          pim += p12.x * wd.y + p12.y * wd.x;
+        if ((tb + u) >= rtiles || row >= rows) continue;
+        const int m1 = static_cast<int>(row / M), m2 = static_cast<int>(row % M);
+#pragma unroll
+        for (int pt = 0; pt < PT; ++pt) {
+          if (!iv[pt]) continue;
+          const double2 p12 = cmul(__ldg(pa[pt] + m1), __ldg(pa[pt] + M + m2));
+          part[pt] += p12.x * acc[u][pt].re[v] - p12.y * acc[u][pt].im[v];
+          if (IM) pim[pt] += p12.x * acd[u][pt].im[v] + p12.y * acd[u][pt].re[v];
         }
       }
   }
-  for (int off = 1; off < 4; off <<= 1) {
-    part.x += __shfl_xor_sync(0xffffffffu, part.x, off);
-    pim += __shfl_xor_sync(0xffffffffu, pim, off);
+#pragma unroll
+  for (int pt = 0; pt < PT; ++pt) {
+    for (int off = 1; off < 4; off <<= 1) {
+      part[pt] += __shfl_xor_sync(0xffffffffu, part[pt], off);
+      if (IM) pim[pt] += __shfl_xor_sync(0xffffffffu, pim[pt], off);
+    }
+    if (tq == 0) red[warp][8 * pt + g] = make_double2(part[pt], pim[pt]);
   }
-  if (tq == 0) red[warp][g] = make_double2(part.x, pim);
   __syncthreads();
-  if (threadIdx.x < 8 && pb + threadIdx.x < p1) {
+  if (threadIdx.x < 8 * PT && pb + threadIdx.x < p1) {
     double2 sum = red[0][threadIdx.x];
     for (int w = 1; w < 4; ++w) {
       sum.x += red[w][threadIdx.x].x;
