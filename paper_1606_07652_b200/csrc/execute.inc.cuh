@@ -186,15 +186,16 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
       const int H = M / 2;
       const long long rtiles = ((long long)M * M + 7) / 8;
       const int smem = (int)(sizeof(double2) * kBigPts * H);
-      dim3 grid((unsigned)np2m, (unsigned)((rtiles + 7) / 8), R);
+      const int rpw = H <= 32 ? 2 : 1;  // row tiles per warp (accumulators: 32 doubles)
+      dim3 grid((unsigned)np2m, (unsigned)((rtiles + 8 * rpw - 1) / (8 * rpw)), R);
       auto lb = [&](auto kern) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         kern<<<grid, 256, smem, st>>>(leaf_list, p->leaf_start.as<int>(), p->pht.as<double2>(),
                                       p->lam.as<double>(), M, K, n, leaf.nbox,
                                       leaf.mult.as<double2>(), H, H);
       };
-      if (H <= 32) lb(k_p2m_big<4>);
-      else lb(k_p2m_big<8>);
+      if (H <= 32) lb(k_p2m_big<4, 2>);
+      else lb(k_p2m_big<8, 1>);
       const int smx = (int)(sizeof(double2) * kBigPts * 64);
       CK(cudaFuncSetAttribute(k_p2m_axes, cudaFuncAttributeMaxDynamicSharedMemorySize, smx));
       k_p2m_axes<<<dim3((unsigned)np2m, 3, R), 256, smx, st>>>(

@@ -588,7 +588,7 @@ constexpr int kBigPts = 64;  // points per CTA (P2M: leaf chunk; L2P: span)
 
 // P2M: V[(m1, m2)][m3] = sum_j conj(P1_j[m1] P2_j[m2]) lambda_j conj(P3_j[m3]),
 // warp w: row tile 8 blockIdx.y + w (8 warps), all ceil(M / 8) column tiles.
-template <int MCT>
+template <int MCT, int RPW = 1>
 __global__ void __launch_bounds__(256, 1)
     k_p2m_big(const int* __restrict__ leaf_list, const int* __restrict__ leaf_start,
               const double2* __restrict__ pht, const double* __restrict__ lam, int M,
@@ -603,15 +603,25 @@ __global__ void __launch_bounds__(256, 1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tq = lane & 3;
   const long long rows = (long long)M * M;
-  const long long row = (8LL * blockIdx.y + warp) * 8 + g;  // this lane's A row
-  const bool rv = row < rows;
-  const int m1 = rv ? static_cast<int>(row / M) : 0, m2 = rv ? static_cast<int>(row % M) : 0;
+  // RPW row tiles per warp: tiles (8 blockIdx.y + warp) RPW + q
+  long long row[RPW];
+  bool rv[RPW];
+  int m1[RPW], m2[RPW];
+#pragma unroll
+  for (int q = 0; q < RPW; ++q) {
+    row[q] = ((8LL * blockIdx.y + warp) * RPW + q) * 8 + g;  // this lane's A row
+    rv[q] = row[q] < rows;
+    m1[q] = rv[q] ? static_cast<int>(row[q] / M) : 0;
+    m2[q] = rv[q] ? static_cast<int>(row[q] % M) : 0;
+  }
   const int p0 = leaf_start[a], p1 = leaf_start[a + 1];
   const double* lr = lam + (long long)r * n;
   const int per = 3 * M;
-  CTile acc[MCT];
+  CTile acc[RPW][MCT];
 #pragma unroll
-  for (int u = 0; u < MCT; ++u) acc[u] = CTile{{0.0, 0.0}, {0.0, 0.0}};
+  for (int q = 0; q < RPW; ++q)
+#pragma unroll
+    for (int u = 0; u < MCT; ++u) acc[q][u] = CTile{{0.0, 0.0}, {0.0, 0.0}};
   for (int c0 = p0; c0 < p1; c0 += kBigPts) {
     const int nb = min(kBigPts, p1 - c0);
     __syncthreads();
@@ -625,29 +635,35 @@ __global__ void __launch_bounds__(256, 1)
     for (int j0 = 0; j0 < nb; j0 += 4) {
       const int j = j0 + tq;
       const bool jv = j < nb;
-      double2 za = make_double2(0.0, 0.0);
-      if (jv && rv) {
-        const double2* pj = pht + (long long)(c0 + j) * per;
-        za = cmul(__ldg(pj + m1), __ldg(pj + M + m2));
-      }
-      const double are = za.x, aim = -za.y;  // conj(P1 P2)
+      double2 bv[MCT];
 #pragma unroll
       for (int u = 0; u < MCT; ++u) {
         const int col = 8 * u + g;
-        const double2 b = (jv && col < ncol) ? s3[j * ncol + col] : make_double2(0.0, 0.0);
-        cdmma(acc[u], are, aim, -aim, b.x, b.y);
+        bv[u] = (jv && col < ncol) ? s3[j * ncol + col] : make_double2(0.0, 0.0);
+      }
+      const double2* pj = pht + (long long)(c0 + (jv ? j : 0)) * per;
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) {
+        double2 za = make_double2(0.0, 0.0);
+        if (jv && rv[q]) za = cmul(__ldg(pj + m1[q]), __ldg(pj + M + m2[q]));
+        const double are = za.x, aim = -za.y;  // conj(P1 P2)
+#pragma unroll
+        for (int u = 0; u < MCT; ++u) cdmma(acc[q][u], are, aim, -aim, bv[u].x, bv[u].y);
       }
     }
   }
   double2* out = mult + ((long long)r * nleaf + a) * K;
-  const long long orow = (8LL * blockIdx.y + warp) * 8 + g;  // C row = g
-  if (orow >= rows) return;
 #pragma unroll
-  for (int u = 0; u < MCT; ++u) {
+  for (int q = 0; q < RPW; ++q) {
+    const long long orow = row[q];  // C row = g
+    if (orow >= rows) continue;
 #pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      const int col = 8 * u + 2 * tq + v;
-      if (col < ncol) out[orow * ncol + col] = make_double2(acc[u].re[v], acc[u].im[v]);
+    for (int u = 0; u < MCT; ++u) {
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int col = 8 * u + 2 * tq + v;
+        if (col < ncol) out[orow * ncol + col] = make_double2(acc[q][u].re[v], acc[q][u].im[v]);
+      }
     }
   }
 }
