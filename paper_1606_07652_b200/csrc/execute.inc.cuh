@@ -26,8 +26,14 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
   }
   geo.L = L;
   const bool profiling = p->profiling && phase == 0;
+  // NVTX ranges name the stages' launch issue on the host timeline (nsys / ncu)
+  static const char* const kStage[BLFMM_NSTAGES + 1] = {
+      "blfmm gather", "blfmm p2m", "blfmm m2m", "blfmm m2l+l2l", "blfmm l2p", "blfmm near",
+      "blfmm combine", "blfmm end"};
   auto mark = [&](int i) {
     if (profiling) CK(cudaEventRecord(p->ev[i], st));
+    if (i > 0) nvtxRangePop();
+    if (i < BLFMM_NSTAGES) nvtxRangePushA(kStage[i]);
   };
   const bool up = phase != 2, down = phase != 1;
   if (up) for (int i = 0; i < BLFMM_NSTAGES; ++i) p->times.launches[i] = 0;
@@ -334,6 +340,7 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
           p->node_m.as<int>(), mult_ptr(p, l - 1));
     }
     CK(cudaGetLastError());
+    nvtxRangePop();  // the upsweep half ends here (exchange mode)
     return;
   }
   mark(3);
