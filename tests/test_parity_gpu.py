@@ -725,3 +725,31 @@ def test_half_spectrum_general_even_m_batched(blfmm, oracle):
     rf, _ = gpu_mlfmm(blfmm, x, w, W.kernel, W.sigma, 24, 3, tuning={"half_spectrum": 0})
     assert "k_p2m_axes" in ph.kernels()["p2m"]
     assert rel_l2(rh.values, rf.values) <= 1e-13
+
+
+@pytest.mark.parametrize("d,m,nrhs", [(3, 16, 1), (3, 20, 1), (2, 16, 1), (3, 16, 8), (3, 58, 1)])
+@pytest.mark.parametrize("n", [0, 1, 2, 37])
+def test_edge_cases_round2_kernels(blfmm, oracle, d, m, nrhs, n):
+    """Empty, single-point and tiny inputs (with clamp-edge coordinates and a
+    duplicate) on the round-2 kernels: column couple, 2-D generated-phase
+    DMMA P2M / L2P, the general half spectrum, the multi-RHS GEMMs and the
+    DMMA near field."""
+    rng = np.random.default_rng(11 + n)
+    x = rng.random((n, d))
+    if n >= 2:
+        x[0] = 0.0
+        x[1] = 1.0
+    if n >= 37:
+        x[36] = x[35]
+    w = rng.uniform(-1, 1, (nrhs, n)) if nrhs > 1 else rng.uniform(-1, 1, n)
+    spec = "imq:c=0.1" if d == 3 else "mq:c=0.05"
+    res, plan = gpu_mlfmm(blfmm, x, w, spec, math.pi, m, 3)
+    vals = np.asarray(res.values).reshape(nrhs, n)
+    if n == 0:
+        assert vals.size == 0 and res.stats.near_pairs == 0
+        return
+    ov, ost, _ = oracle.mlfmm(x, w, spec, math.pi, m, 3)
+    ov = np.asarray(ov).reshape(nrhs, n)
+    for r in range(nrhs):
+        assert rel_l2(vals[r], ov[r]) <= TOL, (r, rel_l2(vals[r], ov[r]))
+    assert res.stats.near_pairs == ost["near_pairs"]
