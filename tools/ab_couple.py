@@ -40,9 +40,12 @@ def run(W, x, w, leaf, var, steps=10):
 
 
 def main():
-    vars_ = [int(a) for a in sys.argv[1:]] or [0, 1, 2, 3, 4]
+    only = [a for a in sys.argv[1:] if not a.lstrip("-").isdigit()]
+    vars_ = [int(a) for a in sys.argv[1:] if a.lstrip("-").isdigit()] or [0, 1, 2, 3, 4]
     for name, n, leaf in [("P3", None, 6), ("P3", 200000, 5), ("P2p", None, 4), ("P5", None, 4),
                           ("P2", None, 4)]:
+        if only and name not in only:
+            continue
         W = I.WORKLOADS[name]
         x, w = W.make(n) if n else W.make()
         base = None
