@@ -19,6 +19,9 @@ HOST_CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["blfmm.cu", "krylov.cu"]
 CPP_SOURCES = ["spectrum.cpp"]
+# development builds only: BLFMM_DEV_KNOBS=1 compiles the A/B experiment
+# switches (plan->xp[], read from BLFMM_XP0..3); the product build has none
+DEV_FLAGS = ["-DBLFMM_DEV_KNOBS"] if os.environ.get("BLFMM_DEV_KNOBS") == "1" else []
 
 
 def _sources():
@@ -51,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(bdir, src + ".o")
         cmd = [NVCC, "-ccbin", HOST_CXX, "-std=c++17", "-O3", "-lineinfo", *ARCH,
                "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
-               "-c", os.path.join(CSRC, src), "-o", obj]
+               *DEV_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         _run(cmd, verbose, log=os.path.join(bdir, src + ".ptxas.log"))
         objs.append(obj)
     tmp = LIB + ".tmp"

@@ -191,17 +191,17 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
       // half), blocks C / B1 / B2 as three small GEMMs
       const int H = M / 2;
       const long long rtiles = ((long long)M * M + 7) / 8;
-      const int smem = (int)(sizeof(double2) * kBigPts * H);
-      const int rpw = H <= 32 ? 2 : 1;  // row tiles per warp (accumulators: 32 doubles)
-      dim3 grid((unsigned)np2m, (unsigned)((rtiles + 8 * rpw - 1) / (8 * rpw)), R);
-      auto lb = [&](auto kern) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        kern<<<grid, 256, smem, st>>>(leaf_list, p->leaf_start.as<int>(), p->pht.as<double2>(),
-                                      p->lam.as<double>(), M, K, n, leaf.nbox,
-                                      leaf.mult.as<double2>(), H, H);
-      };
-      if (H <= 32) lb(k_p2m_big<4, 2>);
-      else lb(k_p2m_big<8, 1>);
+      // block A: 3M DMMA, B staged once per (leaf, row-tile group); H <= 32
+      // always holds here (even M <= 64)
+      {
+        constexpr int kGroups = 2;
+        const int sm3 = (int)(sizeof(double) * 3 * kBig3Pts * kBig3CS);
+        auto kern = k_p2m_big3<1, 8, 2>;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3));
+        kern<<<dim3((unsigned)(np2m * kGroups), 1, R), 256, sm3, st>>>(
+            leaf_list, p->leaf_start.as<int>(), p->pht.as<double2>(), p->lam.as<double>(), M, K, n,
+            leaf.nbox, leaf.mult.as<double2>(), H, H, kGroups);
+      }
       const int smx = (int)(sizeof(double2) * kBigPts * 64);
       CK(cudaFuncSetAttribute(k_p2m_axes, cudaFuncAttributeMaxDynamicSharedMemorySize, smx));
       k_p2m_axes<<<dim3((unsigned)np2m, 3, R), 256, smx, st>>>(
@@ -549,7 +549,27 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
             p->himag.as<double>(), p->imag_bits.as<unsigned long long>());
       };
       if (p->want_imag) la(k_l2p_half_a<2, 1, true>, p->work8, p->nwork8);
-      else la(k_l2p_half_a<2, 4, false>, p->work32, p->nwork32);
+      else {
+        // stats-free block A: 3M DMMA on class-sorted spans (<= 64 points)
+        auto la3 = [&](auto kern, int c, long long off) {
+          if (!p->nwork_ha[c]) return;
+          const int npt = 2 * (c + 1);
+          const int smem = (int)(sizeof(double2) * (8 * npt * kHA3CS + 8 * 2 * 8 * kHA3CS) +
+                                 sizeof(double) * (8 * 8 * npt + 8 * npt * kHA3CS));
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          kern<<<dim3((unsigned)p->nwork_ha[c], 1, R), 256, smem, st>>>(
+              p->work_ha.as<int4>() + off, p->leaf_start.as<int>(), p->pht.as<double2>(),
+              leaf.loc.as<double2>(), M, K, n, leaf.nbox, p->weight, p->far_.as<double>());
+        };
+        long long off = 0;
+        la3(k_l2p_half_a3<2>, 0, off);
+        off += p->nwork_ha[0];
+        la3(k_l2p_half_a3<4>, 1, off);
+        off += p->nwork_ha[1];
+        la3(k_l2p_half_a3<6>, 2, off);
+        off += p->nwork_ha[2];
+        la3(k_l2p_half_a3<8>, 3, off);
+      }
     } else if (D == 3 && p->h16) {
       dim3 grid((unsigned)p->nwork128, 1, R);
       // the D-weighted GEMM of max|Im| only when the caller asked for stats

@@ -667,3 +667,126 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
 }
+
+// Large-M P2M of a column window of at most 32 columns (block A of the half
+// spectrum) in the 3-multiplication complex form: 3 real DMMAs per complex tile
+// step instead of 4 (k_l2p_h16S's scheme). A CTA takes a leaf and a group of
+// its row tiles: the B operand lambda conj(P3) of up to kBig3Pts points is
+// staged ONCE as three real planes (b_r, b_i - b_r, b_r + b_i; row stride 36
+// doubles = conflict-free quarter-warp LDS.64; zero filled beyond the leaf's
+// points and the column window, so the contraction carries no predicates),
+// then the warps loop over the group's row tiles (RPW per warp and pass); the
+// A operand conj(P1 P2) of the next k step is loaded while the current one is
+// contracted. k_p2m_big staged B once per 128 rows (27 times per P2 leaf) and
+// waited on it: P2 P2M 11.9 -> see DESIGN.md §4. Leaves of more than kBig3Pts
+// points take further chunks that add to the stored sums (same CTA, in order).
+constexpr int kBig3CS = 36;   // plane row stride (doubles), = 4 mod 16
+constexpr int kBig3Pts = 96;  // points per staged chunk
+template <int RPW, int NW, int MINB>
+__global__ void __launch_bounds__(32 * NW, MINB)
+    k_p2m_big3(const int* __restrict__ leaf_list, const int* __restrict__ leaf_start,
+               const double2* __restrict__ pht, const double* __restrict__ lam, int M,
+               long long K, long long n, long long nleaf, double2* __restrict__ mult, int coff,
+               int ncol, int ngroup) {
+  constexpr int MCT = 4;
+  extern __shared__ __align__(16) double big3_dyn[];  // [3][kBig3Pts][kBig3CS]
+  double* const sr = big3_dyn;
+  double* const sd = sr + kBig3Pts * kBig3CS;
+  double* const ss = sd + kBig3Pts * kBig3CS;
+  const long long li = blockIdx.x / ngroup;
+  const int grp = static_cast<int>(blockIdx.x - li * ngroup);
+  const long long a = leaf_list ? leaf_list[li] : li;
+  const int r = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int rows = M * M, rtiles = (rows + 7) / 8;
+  // this group's row tiles [t_lo, t_hi), in passes of NW * RPW tiles
+  const int per_grp = (rtiles + ngroup - 1) / ngroup;
+  const int t_lo = grp * per_grp, t_hi = min(rtiles, t_lo + per_grp);
+  const int p0 = leaf_start[a], p1 = leaf_start[a + 1];
+  const double* lr = lam + (long long)r * n;
+  const int per = 3 * M;
+  double2* const out = mult + ((long long)r * nleaf + a) * K;
+  for (int c0 = p0; c0 < p1; c0 += kBig3Pts) {
+    const int nb = min(kBig3Pts, p1 - c0), nb4 = (nb + 3) & ~3;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nb4 * 32; t += blockDim.x) {
+      const int j = t >> 5, c = t & 31;
+      double br = 0.0, bi = 0.0;
+      if (j < nb && c < ncol) {
+        const double2 z = __ldg(pht + (long long)(c0 + j) * per + 2 * M + coff + c);
+        const double w = __ldg(lr + c0 + j);
+        br = w * z.x;
+        bi = -w * z.y;
+      }
+      sr[j * kBig3CS + c] = br;
+      sd[j * kBig3CS + c] = bi - br;
+      ss[j * kBig3CS + c] = br + bi;
+    }
+    __syncthreads();
+    for (int tb = t_lo + warp * RPW; tb < t_hi; tb += NW * RPW) {
+      int m1[RPW], m2[RPW], row[RPW];
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) {
+        row[q] = (tb + q) * 8 + g;  // this lane's A row
+        // rows past the group / the grid: any finite A, never stored
+        const int rc = (tb + q < t_hi && row[q] < rows) ? row[q] : 0;
+        m1[q] = rc / M;
+        m2[q] = rc - m1[q] * M;
+      }
+      CTile3 acc[RPW][MCT];
+#pragma unroll
+      for (int q = 0; q < RPW; ++q)
+#pragma unroll
+        for (int u = 0; u < MCT; ++u) acc[q][u] = kZeroTile3;
+      double2 a1[RPW], a2[RPW];
+      auto load_a = [&](int j0) {
+        const double2* pj = pht + (long long)(c0 + min(j0 + tq, nb - 1)) * per;
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+          a1[q] = __ldg(pj + m1[q]);
+          a2[q] = __ldg(pj + M + m2[q]);
+        }
+      };
+      load_a(0);
+      for (int j0 = 0; j0 < nb; j0 += 4) {
+        double are[RPW], aim[RPW];
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+          const double2 za = cmul(a1[q], a2[q]);
+          are[q] = za.x;
+          aim[q] = -za.y;  // conj(P1 P2)
+        }
+        if (j0 + 4 < nb) load_a(j0 + 4);
+        const int o = (j0 + tq) * kBig3CS + g;
+#pragma unroll
+        for (int u = 0; u < MCT; ++u) {
+          const double br = sr[o + 8 * u], bd = sd[o + 8 * u], bs = ss[o + 8 * u];
+#pragma unroll
+          for (int q = 0; q < RPW; ++q)
+            cdmma3(acc[q][u], are[q] + aim[q], are[q], aim[q], br, bd, bs);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) {
+        if (tb + q >= t_hi || row[q] >= rows) continue;
+        double2* orow = out + (long long)row[q] * ncol;  // C row = g
+#pragma unroll
+        for (int u = 0; u < MCT; ++u) {
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int col = 8 * u + 2 * tq + v;
+            if (col >= ncol) continue;
+            double2 w = ctile3_get(acc[q][u], v);
+            if (c0 > p0) {
+              const double2 old = orow[col];
+              w.x += old.x;
+              w.y += old.y;
+            }
+            orow[col] = w;
+          }
+        }
+      }
+    }
+  }
+}

@@ -267,3 +267,119 @@ __global__ void __launch_bounds__(128)
     }
   }
 }
+
+// Block-A L2P (no imaginary residual) for a span of up to 8 NPT points of one
+// leaf per CTA (8 warps; the plan cuts a leaf into equal spans of <= 64 points
+// and sorts them into classes NPT = 2, 4, 6, 8 by their tile count: one launch
+// per class, no predicates in the contraction loop), in the 3-multiplication complex form (3 real DMMAs
+// per complex tile step; k_l2p_h16S's scheme). The span's P3 phases (upper m3
+// half) are staged once in shared memory (rows padded to 36 complex: the
+// quarter-warp LDS.128 fragment loads are conflict-free, zeros beyond H; plus
+// a plane of the 3M operand sums P3_r + P3_i), and
+// every warp streams its row tiles of the leaf's local expansion (8 rows x H
+// complex, contiguous) through a private double buffer with cp.async, one
+// tile ahead: each local is read once per span, and no fragment load waits on
+// global memory. W_i[row] = sum_{m3 >= H} P3_i[m3] L[row][m3 - H], then
+// u_i += w Re sum_row P1_i[m1] P2_i[m2] W_i[row] (added to k_l2p_axes' far_).
+constexpr int kHA3CS = 36;  // row stride (complex) of the staged phases / local tiles
+template <int NPT>
+__global__ void __launch_bounds__(256, NPT <= 4 ? 2 : 1)
+    k_l2p_half_a3(const int4* __restrict__ work, const int* __restrict__ leaf_start,
+                  const double2* __restrict__ pht, const double2* __restrict__ loc, int M,
+                  long long K, long long n, long long nleaf, double weight,
+                  double* __restrict__ far_) {
+  extern __shared__ __align__(16) double2 ha3_dyn[];
+  double2* const zsm = ha3_dyn;                          // [8 NPT][kHA3CS]
+  double2* const lsm = zsm + 8 * NPT * kHA3CS;           // [8 warps][2][8][kHA3CS]
+  double* const red = reinterpret_cast<double*>(lsm + 8 * 2 * 8 * kHA3CS);  // [8][8 NPT]
+  double* const zss = red + 8 * 8 * NPT;  // [8 NPT][kHA3CS] P3_r + P3_i (the 3M operand sum)
+  const int4 item = work[blockIdx.x];  // (leaf, first point, end point, -)
+  const long long lf = item.x;
+  const int r = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int H = M / 2;
+  const int rows = M * M, rtiles = (rows + 7) / 8;
+  const int pb = item.y, p1 = item.z;
+  const int np = p1 - pb;  // <= 8 NPT (the item's class); padded point rows are zero
+  const int per = 3 * M;
+  const double2 zero = make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < 8 * NPT * kHA3CS; t += blockDim.x) {
+    const int j = t / kHA3CS, c = t - j * kHA3CS;
+    const double2 z =
+        (j < np && c < H) ? __ldg(pht + (long long)(pb + j) * per + 2 * M + H + c) : zero;
+    zsm[t] = z;
+    zss[t] = z.x + z.y;
+  }
+  double2* const lbuf = lsm + warp * (2 * 8 * kHA3CS);
+  for (int t = lane; t < 2 * 8 * kHA3CS; t += 32) lbuf[t] = zero;  // pad columns stay zero
+  __syncthreads();
+  const double2* la = loc + ((long long)r * nleaf + lf) * K;
+  // stage row tile tb of the local expansion into buffer b (rows past the
+  // grid re-read row 0: finite, never used)
+  auto stage = [&](int b, int tb) {
+    double2* dst = lbuf + b * (8 * kHA3CS);
+    for (int t = lane; t < 8 * H; t += 32) {
+      const int rr = t / H, c = t - rr * H;
+      const int row = tb * 8 + rr;
+      cp_async16(dst + rr * kHA3CS + c, la + (long long)(row < rows ? row : 0) * H + c);
+    }
+    cp_async_commit();
+  };
+  const double2* pa[NPT];
+#pragma unroll
+  for (int pt = 0; pt < NPT; ++pt) pa[pt] = pht + (long long)min(pb + 8 * pt + g, p1 - 1) * per;
+  double part[NPT];
+#pragma unroll
+  for (int pt = 0; pt < NPT; ++pt) part[pt] = 0.0;
+  int buf = 0;
+  if (warp < rtiles) stage(0, warp);
+  for (int tb = warp; tb < rtiles; tb += 8, buf ^= 1) {
+    if (tb + 8 < rtiles) {
+      stage(buf ^ 1, tb + 8);
+      cp_async_wait_group<1>();
+    } else {
+      cp_async_wait_group<0>();
+    }
+    __syncwarp();
+    CTile3 acc[NPT];
+#pragma unroll
+    for (int pt = 0; pt < NPT; ++pt) acc[pt] = kZeroTile3;
+    const double2* lt = lbuf + buf * (8 * kHA3CS) + g * kHA3CS + tq;
+    const double2* zt = zsm + g * kHA3CS + tq;
+    const double* zst = zss + g * kHA3CS + tq;
+    for (int k0 = 0; k0 < H; k0 += 4) {
+      const double2 lv = lt[k0];
+      const double bd = lv.y - lv.x, bs = lv.x + lv.y;
+#pragma unroll
+      for (int pt = 0; pt < NPT; ++pt) {
+        const double2 z = zt[pt * 8 * kHA3CS + k0];
+        cdmma3(acc[pt], zst[pt * 8 * kHA3CS + k0], z.x, z.y, lv.x, bd, bs);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int row = tb * 8 + 2 * tq + v;
+      if (row >= rows) continue;
+      const int m1 = row / M, m2 = row - m1 * M;
+#pragma unroll
+      for (int pt = 0; pt < NPT; ++pt) {
+        const double2 p12 = cmul(__ldg(pa[pt] + m1), __ldg(pa[pt] + M + m2));
+        const double2 w = ctile3_get(acc[pt], v);
+        part[pt] += p12.x * w.x - p12.y * w.y;
+      }
+    }
+    __syncwarp();  // every lane is done with buffer `buf` before it is refilled
+  }
+#pragma unroll
+  for (int pt = 0; pt < NPT; ++pt) {
+    for (int off = 1; off < 4; off <<= 1) part[pt] += __shfl_xor_sync(0xffffffffu, part[pt], off);
+    if (tq == 0) red[warp * (8 * NPT) + 8 * pt + g] = part[pt];
+  }
+  __syncthreads();
+  if (threadIdx.x < np) {
+    double sum = red[threadIdx.x];
+    for (int w = 1; w < 8; ++w) sum += red[w * (8 * NPT) + threadIdx.x];
+    far_[(long long)r * n + pb + threadIdx.x] += weight * sum;
+  }
+}

@@ -579,6 +579,29 @@ void plan_build_tree(blfmm_plan* p, const double* coords_host) {
       for (int t = hstart[a]; t < hstart[a + 1]; t += kMRSpan) w64.push_back(make_int2((int)a, t));
     upload(p->work64, w64);
     p->nwork64 = static_cast<long long>(w64.size());
+    // block-A L2P of the general half spectrum (k_l2p_half_a3): spans of up to
+    // 64 points in classes of 2, 4, 6, 8 point tiles (heaviest leaves first
+    // inside a class)
+    {
+      std::vector<int4> wc[4];  // (leaf, first point, end point, -)
+      const int cap = 64;
+      for (long long a : order) {
+        // a leaf's points in equal spans of whole tiles (70 points, cap 64: 40 + 30)
+        const int cnt = hstart[a + 1] - hstart[a];
+        const int nsp = (cnt + cap - 1) / cap;
+        const int len = nsp ? ((cnt + nsp - 1) / nsp + 7) / 8 * 8 : 0;
+        for (int t = hstart[a]; t < hstart[a + 1]; t += len) {
+          const int end = std::min(t + len, hstart[a + 1]);
+          wc[((end - t + 7) / 8 - 1) / 2].push_back(make_int4((int)a, t, end, 0));
+        }
+      }
+      std::vector<int4> all;
+      for (int c = 0; c < 4; ++c) {
+        p->nwork_ha[c] = static_cast<long long>(wc[c].size());
+        all.insert(all.end(), wc[c].begin(), wc[c].end());
+      }
+      upload(p->work_ha, all);
+    }
     // parents of the leaves (level L-1) by decreasing point count: the fused
     // P2M + leaf-M2M kernel's work list
     if (L >= 2 && p->lev[L - 1].nbox) {
@@ -689,6 +712,12 @@ void create_plan(const blfmm_plan_desc* desc, const blfmm_tuning* tune, blfmm_pl
   auto t0 = std::chrono::steady_clock::now();
   DeviceGuard guard(desc->device);
   std::unique_ptr<blfmm_plan> p(new blfmm_plan());
+#ifdef BLFMM_DEV_KNOBS
+  for (int i = 0; i < 4; ++i) {
+    const std::string nm = "BLFMM_XP" + std::to_string(i);
+    if (const char* e = std::getenv(nm.c_str())) p->xp[i] = std::atoi(e);
+  }
+#endif
   CK(cudaGetDevice(&p->device));
   CK(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device));
   // Deep 3-D trees (leaf level >= 6, one right-hand side): the register-bound
@@ -954,7 +983,7 @@ void create_plan(const blfmm_plan_desc* desc, const blfmm_tuning* tune, blfmm_pl
     else if (p->mr) k += "k_p2m_mr";
     else if (p->h16 && p->n_p2m_plist > 0) k += "k_p2m_m2m_h16";
     else if (p->h16) k += "k_p2m_h16w4";
-    else if (p->herm) k += "k_p2m_big(half)+k_p2m_axes";
+    else if (p->herm) k += "k_p2m_big3+k_p2m_axes";
     else if (p->g2d16) k += "k_p2m_2d16";
     else if (d == 3 && p->M >= 24 && p->M <= 64 && !p->scaled) k += "k_p2m_big";
     else k += "k_p2m_mma";
@@ -968,7 +997,7 @@ void create_plan(const blfmm_plan_desc* desc, const blfmm_tuning* tune, blfmm_pl
     k += d == 1 ? " l2p=k_l2p"
                 : (p->mr ? " l2p=k_l2p_mr"
                          : (p->h16 ? " l2p=k_l2p_h16S"
-                                   : p->herm ? " l2p=k_l2p_axes+k_l2p_half_a"
+                                   : p->herm ? " l2p=k_l2p_axes+k_l2p_half_a3"
                                     : (p->g2d16 ? " l2p=k_l2p_2d16" : " l2p=k_l2p_mma")));
     if (p->R == 1)
       k += " near=k_near_all(ctas_per_sm=" + std::to_string(p->near_persist) +

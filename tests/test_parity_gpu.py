@@ -716,6 +716,36 @@ def test_half_spectrum_general_even_m(blfmm, oracle, spec, m, n, leaf):
         assert np.linalg.norm(eh - ef) <= 1e-12 * np.linalg.norm(ef)
 
 
+@pytest.mark.parametrize("spec,m,n,leaf", [("imq:c=0.1", 20, 6000, 2), ("gaussian:c=64", 58, 3000, 2)])
+def test_half_spectrum_stats_free_3m_kernels(blfmm, oracle, spec, m, n, leaf):
+    """The stats-free matvec of the general half spectrum (what a Krylov loop
+    and the bench time) runs block A on the 3-multiplication DMMA kernels
+    (k_p2m_big3: B staged once per leaf group, chunks of 96 points;
+    k_l2p_half_a3: class-sorted spans of <= 64 points). Blob inputs at a shallow
+    leaf level give leaves of several hundred points (multi-chunk P2M sums,
+    multi-span L2P, every span class). Equal to the stats-requesting call
+    (4-multiplication L2P) to rounding and to the oracle at the bar."""
+    import torch
+    W = I.WORKLOADS["P3"]
+    x, w = W.make(n)
+    sigma = math.pi
+    res, plan = gpu_mlfmm(blfmm, x, w, spec, sigma, m, leaf)
+    k = plan.kernels()
+    assert k["p2m"] == "k_p2m_big3+k_p2m_axes" and k["l2p"] == "k_l2p_axes+k_l2p_half_a3", k
+    lam = torch.from_numpy(np.ascontiguousarray(w.reshape(1, -1))).cuda()
+    out = torch.empty_like(lam)
+    for _ in range(2):  # direct launch, then the captured graph
+        out.zero_()
+        assert plan.execute_device(lam.data_ptr(), out.data_ptr(), stats=False) is None
+        torch.cuda.synchronize()
+        u = out.cpu().numpy()[0]
+        assert rel_l2(u, res.values) <= 1e-13, rel_l2(u, res.values)
+    ctab = blfmm.translation_coefficients(blfmm.parse_kernel_spec(spec),
+                                          blfmm.make_quadrature(sigma, m, 3)).c_vals
+    ov, _, _ = oracle.mlfmm(x, w, spec, sigma, m, leaf, c_table_in=ctab)
+    assert rel_l2(u, ov) <= TOL, rel_l2(u, ov)
+
+
 def test_half_spectrum_general_even_m_batched(blfmm, oracle):
     """The general half spectrum with several right-hand sides (grid.z = R)."""
     W = I.WORKLOADS["P5"]

@@ -119,7 +119,7 @@ def test_p2_full_size_matches_oracle_on_target_subset(blfmm, oracle):
     x, w = W.make()
     plan = production_plan(blfmm, W, x)
     k = plan.kernels()
-    assert k["p2m"] == "k_p2m_big(half)+k_p2m_axes" and k["l2p"] == "k_l2p_axes+k_l2p_half_a", k
+    assert k["p2m"] == "k_p2m_big3+k_p2m_axes" and k["l2p"] == "k_l2p_axes+k_l2p_half_a3", k
     assert plan.info().stored_nodes < 58 ** 3  # Hermitian half spectrum
     assert k["couple"] == "k_root+k_couple_col<2x2,z32>", k
     assert k["near"].startswith("k_near_all(") and plan.info().near_sym_items > 0, k
