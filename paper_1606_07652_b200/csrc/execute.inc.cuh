@@ -63,7 +63,8 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
       const unsigned gp = (unsigned)(p->num_sms * (p->profiling ? 5 : p->near_persist));
       auto launchp = [&](auto kern) {
         kern<<<gp, 32 * kNearWarps, 0, sn>>>(
-            p->near_ctr.as<unsigned long long>(), p->sym_work.as<int4>(), ns,
+            p->near_ctr.as<unsigned long long>(), p->sym_work.as<int4>(),
+            p->sym_q.as<unsigned char>(), ns,
             p->sym_planes.as<double>(), p->near_work2.as<int2>(), p->nwork2,
             leaf.key.as<uint32_t>(), p->leaf_start.as<int>(), leaf.slotmap.as<int>(),
             p->src4.as<double4>(), L, p->kern.shape, n, p->near_.as<double>(),
@@ -551,24 +552,26 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
       if (p->want_imag) la(k_l2p_half_a<2, 1, true>, p->work8, p->nwork8);
       else {
         // stats-free block A: 3M DMMA on class-sorted spans (<= 64 points)
-        auto la3 = [&](auto kern, int c, long long off) {
+        auto la3 = [&](auto kern, int c, int ng, long long off) {
           if (!p->nwork_ha[c]) return;
           const int npt = 2 * (c + 1);
-          const int smem = (int)(sizeof(double2) * (8 * npt * kHA3CS + 8 * 2 * 8 * kHA3CS) +
+          const int smem = (int)(sizeof(double2) * (8 * npt * kHA3CS + 8 * ng * 2 * 8 * kHA3CS) +
                                  sizeof(double) * (8 * 8 * npt + 8 * npt * kHA3CS));
           CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-          kern<<<dim3((unsigned)p->nwork_ha[c], 1, R), 256, smem, st>>>(
+          kern<<<dim3((unsigned)p->nwork_ha[c], 1, R), 256 * ng, smem, st>>>(
               p->work_ha.as<int4>() + off, p->leaf_start.as<int>(), p->pht.as<double2>(),
               leaf.loc.as<double2>(), M, K, n, leaf.nbox, p->weight, p->far_.as<double>());
         };
         long long off = 0;
-        la3(k_l2p_half_a3<2>, 0, off);
+        la3(k_l2p_half_a3<2, 1>, 0, 1, off);
         off += p->nwork_ha[0];
-        la3(k_l2p_half_a3<4>, 1, off);
+        la3(k_l2p_half_a3<4, 1>, 1, 1, off);
         off += p->nwork_ha[1];
-        la3(k_l2p_half_a3<6>, 2, off);
+        la3(k_l2p_half_a3<6, 1>, 2, 1, off);
         off += p->nwork_ha[2];
-        la3(k_l2p_half_a3<8>, 3, off);
+        // (16 warps as two point-tile groups, k_l2p_half_a3<8, 2>, measured
+        // slower: P2 L2P 10.2 -> 11.1 ms)
+        la3(k_l2p_half_a3<8, 1>, 3, 1, off);
       }
     } else if (D == 3 && p->h16) {
       dim3 grid((unsigned)p->nwork128, 1, R);
@@ -581,13 +584,15 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
                                         p->dtab.as<double>(), n, leaf.nbox, p->weight,
                                         p->far_.as<double>(), p->imag_bits.as<unsigned long long>());
     } else if (D == 2 && p->g2d16) {
-      dim3 grid((unsigned)((p->nwork32 + 3) / 4), 1, R);
-      k_l2p_2d16<<<grid, 128, 0, st>>>(p->work32.as<int2>(), p->nwork32, leaf.key.as<uint32_t>(),
-                                       p->leaf_start.as<int>(), x0, x1, leaf.loc.as<double2>(), n,
-                                       leaf.nbox, L, p->lo[0], p->lo[1], side[0], side[1],
-                                       p->sigma, 2.0 * p->sigma / M, p->weight,
+      const bool s32 = p->xp[0] == 1;
+      const long long nw = s32 ? p->nwork32 : p->nwork128;
+      dim3 grid((unsigned)((nw + 3) / 4), 1, R);
+      k_l2p_2d16<<<grid, 128, 0, st>>>((s32 ? p->work32 : p->work128).as<int2>(), nw,
+                                       leaf.key.as<uint32_t>(), p->leaf_start.as<int>(), x0, x1,
+                                       leaf.loc.as<double2>(), n, leaf.nbox, L, p->lo[0], p->lo[1],
+                                       side[0], side[1], p->sigma, 2.0 * p->sigma / M, p->weight,
                                        p->far_.as<double>(),
-                                       p->imag_bits.as<unsigned long long>());
+                                       p->imag_bits.as<unsigned long long>(), s32 ? 32 : kL2PSpan);
     } else {
       constexpr int WN = 4;
       dim3 grid((unsigned)p->nwork8, 1, R);

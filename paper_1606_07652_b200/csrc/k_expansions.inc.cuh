@@ -392,30 +392,71 @@ __global__ void __launch_bounds__(128)
 
 // ------------------------- phases generated in registers (north star: the
 // plane-wave factors e^{i xi_m t} of P2M / L2P are not read from a table)
-// out[m * stride] = e^{i sgn xi_m t}, xi_m = -sigma + m dxi, m = 0..M-1: one
-// sincos for the anchor xi_{16q} t of every run of 16 nodes and one for the
-// step e^{i sgn dxi t}, then complex multiplications (rounding grows ~m ulp
-// within a run: <= 16 ulp, far below the 1e-10 parity bar).
-template <int M>
-__device__ __forceinline__ void phase_run(double t, double sigma, double dxi, double sgn,
-                                          double2* __restrict__ out, int stride) {
-  const double2 st = polar1(sgn * dxi * t);
+// e^{ix} for the small arguments of leaf-relative phases (|x| <= 1/8: Taylor
+// to x^13 / x^14, truncation < 1e-25 relative), the library sincos otherwise.
+__device__ __forceinline__ double2 polar_small(double x) {
+  if (fabs(x) > 0.125) return polar1(x);
+  const double x2 = x * x;
+  double sn = 1.0 / 6227020800.0;        // 1/13!
+  sn = fma(sn, -x2, 1.0 / 39916800.0);   // 1/11!
+  sn = fma(sn, -x2, 1.0 / 362880.0);     // 1/9!
+  sn = fma(sn, -x2, 1.0 / 5040.0);       // 1/7!
+  sn = fma(sn, -x2, 1.0 / 120.0);        // 1/5!
+  sn = fma(sn, -x2, 1.0 / 6.0);          // 1/3!
+  sn = fma(-sn * x2, x, x);
+  double cs = 1.0 / 87178291200.0;       // 1/14!
+  cs = fma(cs, -x2, 1.0 / 479001600.0);  // 1/12!
+  cs = fma(cs, -x2, 1.0 / 3628800.0);    // 1/10!
+  cs = fma(cs, -x2, 1.0 / 40320.0);      // 1/8!
+  cs = fma(cs, -x2, 1.0 / 720.0);        // 1/6!
+  cs = fma(cs, -x2, 1.0 / 24.0);         // 1/4!
+  cs = fma(cs, -x2, 0.5);                // 1/2!
+  cs = fma(-cs, x2, 1.0);
+  return make_double2(cs, sn);
+}
+// The M = 16 phase row e^{i xi_m t}, m = 0..15: the grid -sigma + m dxi has
+// xi_8 = 0 exactly and xi_{16-m} = -xi_m, so the row is the powers of
+// s = e^{i dxi t}: s^{m-8} for m >= 8 and conj(s^{8-m}) below (one sincos,
+// 7 products in a depth-3 tree).
+__device__ __forceinline__ void gen_row16(double tv, double dxi, double2* __restrict__ row) {
+  double2 pw[9];
+  pw[0] = make_double2(1.0, 0.0);
+  pw[1] = polar_small(dxi * tv);
+  pw[2] = cmul(pw[1], pw[1]);
+  pw[3] = cmul(pw[2], pw[1]);
+  pw[4] = cmul(pw[2], pw[2]);
+  pw[5] = cmul(pw[4], pw[1]);
+  pw[6] = cmul(pw[4], pw[2]);
+  pw[7] = cmul(pw[4], pw[3]);
+  pw[8] = cmul(pw[4], pw[4]);
 #pragma unroll
-  for (int q = 0; q < M; q += 16) {
-    double2 z = polar1(sgn * (-sigma + q * dxi) * t);
+  for (int m = 0; m < 16; ++m) row[m] = m >= 8 ? pw[m - 8] : make_double2(pw[8 - m].x, -pw[8 - m].y);
+}
+// gen_row16 with a row stride (the 2-D kernels' [m][point] staging)
+__device__ __forceinline__ void gen_row16s(double tv, double dxi, double2* __restrict__ out,
+                                           int stride) {
+  double2 pw[9];
+  pw[0] = make_double2(1.0, 0.0);
+  pw[1] = polar_small(dxi * tv);
+  pw[2] = cmul(pw[1], pw[1]);
+  pw[3] = cmul(pw[2], pw[1]);
+  pw[4] = cmul(pw[2], pw[2]);
+  pw[5] = cmul(pw[4], pw[1]);
+  pw[6] = cmul(pw[4], pw[2]);
+  pw[7] = cmul(pw[4], pw[3]);
+  pw[8] = cmul(pw[4], pw[4]);
 #pragma unroll
-    for (int m = q; m < q + 16 && m < M; ++m) {
-      out[m * stride] = z;
-      z = cmul(z, st);
-    }
-  }
+  for (int m = 0; m < 16; ++m)
+    out[m * stride] = m >= 8 ? pw[m - 8] : make_double2(pw[8 - m].x, -pw[8 - m].y);
 }
 
 // ----------------------- 2-D, M = 16 (K = 256): P2M / L2P on FP64 DMMA
 // One warp per leaf (P2M) or per 32-point chunk of a leaf (L2P); the point
 // phases of a 16-point chunk are generated by the warp into shared memory
-// (lanes 0-15: axis 0 of one point each, lanes 16-31: axis 1) and read back
-// as DMMA fragments. Row strides are chosen so the fragment reads of a
+// (lanes 0-15: axis 0 of one point each, lanes 16-31: axis 1; gen_row16s: the
+// M = 16 grid is symmetric about xi_8 = 0, so a row is the powers of
+// e^{i dxi t} - one small-angle sincos and 7 products) and read back as DMMA
+// fragments. Row strides are chosen so the fragment reads of a
 // quarter warp hit distinct 16-byte bank groups.
 constexpr int kP2D = 16;      // points per generated chunk
 constexpr int kP2DSA = 20;    // P2M row stride (== 4 mod 8)
@@ -453,14 +494,17 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[i][j] = CTile{{0.0, 0.0}, {0.0, 0.0}};
   const int p0 = leaf_start[a], p1 = leaf_start[a + 1];
+  // the next chunk's coordinate and weight are loaded while this one is contracted
+  double xn = p0 + pl < p1 ? __ldg(xs + p0 + pl) : ctr;
+  double wn = (!half && p0 + pl < p1) ? __ldg(lr + p0 + pl) : 0.0;
   for (int j0 = p0; j0 < p1; j0 += kP2D) {
     {
-      const int j = j0 + pl;
-      const bool jv = j < p1;
-      const double t = jv ? __ldg(xs + j) - ctr : 0.0;
-      phase_run<16>(t, sigma, dxi, -1.0, gen, kP2DSA);  // conj phases
+      const double t = xn - ctr, w = wn;
+      const int jn = j0 + kP2D + pl;
+      xn = jn < p1 ? __ldg(xs + jn) : ctr;
+      wn = (!half && jn < p1) ? __ldg(lr + jn) : 0.0;
+      gen_row16s(-t, dxi, gen, kP2DSA);  // conj phases: e^{-i xi_m t}
       if (!half) {
-        const double w = jv ? __ldg(lr + j) : 0.0;
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
           double2 z = sA[warp][m][pl];
@@ -498,14 +542,17 @@ __global__ void __launch_bounds__(128)
 // W[i][m1] = sum_{m2} P1_i[m2] L[m1][m2] on DMMA (A = P1, 8 points x 4 nodes;
 // B[m2][m1] = L[m1][m2], held in registers for the whole item), then
 // u_i = w Re sum_{m1} P0_i[m1] W[i][m1] on the accumulator fragments.
-// work[item] = (leaf, first point of a <= 32-point chunk).
+// work[item] = (leaf, first point of a span of <= `span` points): a warp keeps
+// the leaf's B fragments for the whole span (128: one load of the local
+// expansion per 64-point leaf; the 32-point items left the kernel waiting on
+// global loads, long-scoreboard 68 % of the stall samples).
 __global__ void __launch_bounds__(128)
     k_l2p_2d16(const int2* __restrict__ work, long long nitems,
                const uint32_t* __restrict__ leaf_key, const int* __restrict__ leaf_start,
                const double* __restrict__ x0, const double* __restrict__ x1,
                const double2* __restrict__ loc, long long n, long long nleaf, int L, double lo0,
                double lo1, double s0, double s1, double sigma, double dxi, double weight,
-               double* __restrict__ far_, unsigned long long* __restrict__ imag_bits) {
+               double* __restrict__ far_, unsigned long long* __restrict__ imag_bits, int span) {
   __shared__ __align__(16) double2 sP0[4][16][kP2DS0];
   __shared__ __align__(16) double2 sP1[4][16][kP2DS1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -530,14 +577,17 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) bl[nt][ks] = __ldg(la + (nt * 8 + g) * 16 + ks * 4 + tq);
   const int p1 = leaf_start[a + 1];
-  const int pend = min(p1, it.y + 32);
+  const int pend = min(p1, it.y + span);
   double* fr = far_ + (long long)r * n;
   double imax = 0.0;
+  // the next chunk's coordinate is loaded while the current chunk is contracted
+  double xn = it.y + pl < pend ? __ldg(xs + it.y + pl) : ctr;
   for (int j0 = it.y; j0 < pend; j0 += kP2D) {
     {
-      const int j = j0 + pl;
-      const double t = j < pend ? __ldg(xs + j) - ctr : 0.0;
-      phase_run<16>(t, sigma, dxi, 1.0, gen, gstride);
+      const double t = xn - ctr;
+      const int jn = j0 + kP2D + pl;
+      xn = jn < pend ? __ldg(xs + jn) : ctr;
+      gen_row16s(t, dxi, gen, gstride);
     }
     __syncwarp();
 #pragma unroll

@@ -33,46 +33,7 @@ __host__ __device__ __forceinline__ void h16_brow(int rb, int& m1, int& m2) {
   m2 = rb < 16 ? rb : 0;
 }
 
-// e^{ix} for the small arguments of leaf-relative phases (|x| <= 1/8: Taylor
-// to x^13 / x^14, truncation < 1e-25 relative), the library sincos otherwise.
-__device__ __forceinline__ double2 polar_small(double x) {
-  if (fabs(x) > 0.125) return polar1(x);
-  const double x2 = x * x;
-  double sn = 1.0 / 6227020800.0;        // 1/13!
-  sn = fma(sn, -x2, 1.0 / 39916800.0);   // 1/11!
-  sn = fma(sn, -x2, 1.0 / 362880.0);     // 1/9!
-  sn = fma(sn, -x2, 1.0 / 5040.0);       // 1/7!
-  sn = fma(sn, -x2, 1.0 / 120.0);        // 1/5!
-  sn = fma(sn, -x2, 1.0 / 6.0);          // 1/3!
-  sn = fma(-sn * x2, x, x);
-  double cs = 1.0 / 87178291200.0;       // 1/14!
-  cs = fma(cs, -x2, 1.0 / 479001600.0);  // 1/12!
-  cs = fma(cs, -x2, 1.0 / 3628800.0);    // 1/10!
-  cs = fma(cs, -x2, 1.0 / 40320.0);      // 1/8!
-  cs = fma(cs, -x2, 1.0 / 720.0);        // 1/6!
-  cs = fma(cs, -x2, 1.0 / 24.0);         // 1/4!
-  cs = fma(cs, -x2, 0.5);                // 1/2!
-  cs = fma(-cs, x2, 1.0);
-  return make_double2(cs, sn);
-}
-// The M = 16 phase row e^{i xi_m t}, m = 0..15: the grid -sigma + m dxi has
-// xi_8 = 0 exactly and xi_{16-m} = -xi_m, so the row is the powers of
-// s = e^{i dxi t}: s^{m-8} for m >= 8 and conj(s^{8-m}) below (one sincos,
-// 7 products in a depth-3 tree).
-__device__ __forceinline__ void gen_row16(double tv, double dxi, double2* __restrict__ row) {
-  double2 pw[9];
-  pw[0] = make_double2(1.0, 0.0);
-  pw[1] = polar_small(dxi * tv);
-  pw[2] = cmul(pw[1], pw[1]);
-  pw[3] = cmul(pw[2], pw[1]);
-  pw[4] = cmul(pw[2], pw[2]);
-  pw[5] = cmul(pw[4], pw[1]);
-  pw[6] = cmul(pw[4], pw[2]);
-  pw[7] = cmul(pw[4], pw[3]);
-  pw[8] = cmul(pw[4], pw[4]);
-#pragma unroll
-  for (int m = 0; m < 16; ++m) row[m] = m >= 8 ? pw[m - 8] : make_double2(pw[8 - m].x, -pw[8 - m].y);
-}
+// (polar_small / gen_row16: k_expansions.inc.cuh, shared with the 2-D kernels)
 struct LeafGeom {  // leaf centre from its Morton key (geometry.hpp:62-64)
   double lo[3], side[3];
   int L;

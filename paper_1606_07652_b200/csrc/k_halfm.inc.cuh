@@ -282,21 +282,26 @@ __global__ void __launch_bounds__(128)
 // global memory. W_i[row] = sum_{m3 >= H} P3_i[m3] L[row][m3 - H], then
 // u_i += w Re sum_row P1_i[m1] P2_i[m2] W_i[row] (added to k_l2p_axes' far_).
 constexpr int kHA3CS = 36;  // row stride (complex) of the staged phases / local tiles
-template <int NPT>
-__global__ void __launch_bounds__(256, NPT <= 4 ? 2 : 1)
+template <int NPT, int NG>
+__global__ void __launch_bounds__(256 * NG, (NG == 1 && NPT <= 4) ? 2 : 1)
     k_l2p_half_a3(const int4* __restrict__ work, const int* __restrict__ leaf_start,
                   const double2* __restrict__ pht, const double2* __restrict__ loc, int M,
                   long long K, long long n, long long nleaf, double weight,
                   double* __restrict__ far_) {
   extern __shared__ __align__(16) double2 ha3_dyn[];
   double2* const zsm = ha3_dyn;                          // [8 NPT][kHA3CS]
-  double2* const lsm = zsm + 8 * NPT * kHA3CS;           // [8 warps][2][8][kHA3CS]
-  double* const red = reinterpret_cast<double*>(lsm + 8 * 2 * 8 * kHA3CS);  // [8][8 NPT]
+  double2* const lsm = zsm + 8 * NPT * kHA3CS;           // [8 NG warps][2][8][kHA3CS]
+  double* const red = reinterpret_cast<double*>(lsm + 8 * NG * 2 * 8 * kHA3CS);  // [8][8 NPT]
   double* const zss = red + 8 * 8 * NPT;  // [8 NPT][kHA3CS] P3_r + P3_i (the 3M operand sum)
   const int4 item = work[blockIdx.x];  // (leaf, first point, end point, -)
   const long long lf = item.x;
   const int r = blockIdx.z;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warp = (point-tile group, row-tile lane): NG groups of NPW point tiles, 8
+  // warps per group striding the row tiles (16 warps keep the DMMA pipe fed
+  // through the fixed-latency waits that 8 warps of 8 tiles left exposed)
+  constexpr int NPW = NPT / NG;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int warp = wid & 7, grp = wid >> 3;
   const int g = lane >> 2, tq = lane & 3;
   const int H = M / 2;
   const int rows = M * M, rtiles = (rows + 7) / 8;
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(256, NPT <= 4 ? 2 : 1)
     zsm[t] = z;
     zss[t] = z.x + z.y;
   }
-  double2* const lbuf = lsm + warp * (2 * 8 * kHA3CS);
+  double2* const lbuf = lsm + wid * (2 * 8 * kHA3CS);
   for (int t = lane; t < 2 * 8 * kHA3CS; t += 32) lbuf[t] = zero;  // pad columns stay zero
   __syncthreads();
   const double2* la = loc + ((long long)r * nleaf + lf) * K;
@@ -326,12 +331,13 @@ __global__ void __launch_bounds__(256, NPT <= 4 ? 2 : 1)
     }
     cp_async_commit();
   };
-  const double2* pa[NPT];
+  const double2* pa[NPW];
 #pragma unroll
-  for (int pt = 0; pt < NPT; ++pt) pa[pt] = pht + (long long)min(pb + 8 * pt + g, p1 - 1) * per;
-  double part[NPT];
+  for (int pt = 0; pt < NPW; ++pt)
+    pa[pt] = pht + (long long)min(pb + 8 * (grp * NPW + pt) + g, p1 - 1) * per;
+  double part[NPW];
 #pragma unroll
-  for (int pt = 0; pt < NPT; ++pt) part[pt] = 0.0;
+  for (int pt = 0; pt < NPW; ++pt) part[pt] = 0.0;
   int buf = 0;
   if (warp < rtiles) stage(0, warp);
   for (int tb = warp; tb < rtiles; tb += 8, buf ^= 1) {
@@ -342,17 +348,17 @@ __global__ void __launch_bounds__(256, NPT <= 4 ? 2 : 1)
       cp_async_wait_group<0>();
     }
     __syncwarp();
-    CTile3 acc[NPT];
+    CTile3 acc[NPW];
 #pragma unroll
-    for (int pt = 0; pt < NPT; ++pt) acc[pt] = kZeroTile3;
+    for (int pt = 0; pt < NPW; ++pt) acc[pt] = kZeroTile3;
     const double2* lt = lbuf + buf * (8 * kHA3CS) + g * kHA3CS + tq;
-    const double2* zt = zsm + g * kHA3CS + tq;
-    const double* zst = zss + g * kHA3CS + tq;
+    const double2* zt = zsm + (grp * NPW * 8 + g) * kHA3CS + tq;
+    const double* zst = zss + (grp * NPW * 8 + g) * kHA3CS + tq;
     for (int k0 = 0; k0 < H; k0 += 4) {
       const double2 lv = lt[k0];
       const double bd = lv.y - lv.x, bs = lv.x + lv.y;
 #pragma unroll
-      for (int pt = 0; pt < NPT; ++pt) {
+      for (int pt = 0; pt < NPW; ++pt) {
         const double2 z = zt[pt * 8 * kHA3CS + k0];
         cdmma3(acc[pt], zst[pt * 8 * kHA3CS + k0], z.x, z.y, lv.x, bd, bs);
       }
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(256, NPT <= 4 ? 2 : 1)
       if (row >= rows) continue;
       const int m1 = row / M, m2 = row - m1 * M;
 #pragma unroll
-      for (int pt = 0; pt < NPT; ++pt) {
+      for (int pt = 0; pt < NPW; ++pt) {
         const double2 p12 = cmul(__ldg(pa[pt] + m1), __ldg(pa[pt] + M + m2));
         const double2 w = ctile3_get(acc[pt], v);
         part[pt] += p12.x * w.x - p12.y * w.y;
@@ -372,9 +378,9 @@ __global__ void __launch_bounds__(256, NPT <= 4 ? 2 : 1)
     __syncwarp();  // every lane is done with buffer `buf` before it is refilled
   }
 #pragma unroll
-  for (int pt = 0; pt < NPT; ++pt) {
+  for (int pt = 0; pt < NPW; ++pt) {
     for (int off = 1; off < 4; off <<= 1) part[pt] += __shfl_xor_sync(0xffffffffu, part[pt], off);
-    if (tq == 0) red[warp * (8 * NPT) + 8 * pt + g] = part[pt];
+    if (tq == 0) red[warp * (8 * NPT) + 8 * (grp * NPW + pt) + g] = part[pt];
   }
   __syncthreads();
   if (threadIdx.x < np) {

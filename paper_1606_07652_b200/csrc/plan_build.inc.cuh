@@ -518,13 +518,21 @@ void plan_build_tree(blfmm_plan* p, const double* coords_host) {
       }
       std::stable_sort(sitems.begin(), sitems.end(),
                        [&](const auto& u, const auto& v) { return u.first < v.first; });
+      // device items carry the point ranges (targets [x, y), sources [z, w))
+      // and the target-side neighbour index separately
       std::vector<int4> sw(sitems.size());
-      for (size_t q = 0; q < sitems.size(); ++q) sw[q] = sitems[q].second;
+      std::vector<unsigned char> sqv(sitems.size());
+      for (size_t q = 0; q < sitems.size(); ++q) {
+        const int4 s = sitems[q].second;
+        sw[q] = make_int4(hstart[s.x], hstart[s.x + 1], hstart[s.y], hstart[s.y + 1]);
+        sqv[q] = static_cast<unsigned char>(s.z);
+      }
       p->nsym = static_cast<long long>(sw.size());
       bool any = false;
       for (long long a = 0; a < leaf.nbox && !any; ++a) any = lmask[a] != 0;
       if (any) {
         upload(p->sym_work, sw);
+        upload(p->sym_q, sqv);
         std::vector<unsigned> pm(n);
         for (long long a = 0; a < leaf.nbox; ++a)
           for (int i = hstart[a]; i < hstart[a + 1]; ++i) pm[i] = lmask[a];

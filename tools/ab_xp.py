@@ -1,7 +1,7 @@
 """A/B of development experiment switches (BLFMM_XP0..3, development builds:
 BLFMM_DEV_KNOBS=1 at build time): one plan per setting of a BASELINE workload,
 stage times of the median step and the result's rel-l2 against the first
-setting.  usage: ab_xp.py WORKLOAD "0,0,0,0" "1,0,1,0" ..."""
+setting.  usage: ab_xp.py WORKLOAD "0,0,0,0" "1,0,1,0:{\"near_ctas_per_sm\": 1}" ..."""
 import os
 import sys
 
@@ -15,14 +15,14 @@ import paper_1606_07652_b200 as B  # noqa: E402
 from paper_1606_07652_b200 import inputs as I  # noqa: E402
 
 
-def run(wl, xp, steps=7):
+def run(wl, xp, steps=7, tuning=None):
     for i, v in enumerate(xp):
         os.environ[f"BLFMM_XP{i}"] = str(v)
     W = I.WORKLOADS[wl]
     x, w = W.make(None)
     n = x.shape[0]
     plan = B.Plan(B.PointSet(W.d, x), W.leaf, B.parse_kernel_spec(W.kernel), W.sigma, W.m,
-                  nrhs=W.nrhs)
+                  nrhs=W.nrhs, tuning=tuning)
     lam = torch.from_numpy(np.ascontiguousarray(w.reshape(W.nrhs, n))).cuda()
     out = torch.empty_like(lam)
     s = torch.cuda.Stream()
@@ -54,8 +54,10 @@ def main():
     wl = sys.argv[1]
     ref = None
     for spec in sys.argv[2:]:
-        xp = [int(v) for v in spec.split(",")]
-        ms, stages, u = run(wl, xp)
+        head, _, tj = spec.partition(":")
+        xp = [int(v) for v in head.split(",")]
+        import json
+        ms, stages, u = run(wl, xp, tuning=json.loads(tj) if tj else None)
         if ref is None:
             ref = u
         err = np.linalg.norm(u - ref) / np.linalg.norm(ref)
