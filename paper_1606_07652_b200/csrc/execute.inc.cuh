@@ -174,7 +174,7 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
                                        p->sigma, 2.0 * p->sigma / M, leaf.mult.as<double2>());
     } else if (D == 3 && p->mr) {
       auto launch_mr = [&](auto kern, int span, int nw) {
-        const int smem = (int)(sizeof(double2) * span * kMRRow + sizeof(double) * span * kMRLam);
+        const int smem = (int)(sizeof(double2) * span * kMRRowP + sizeof(double) * span * kMRLam);
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         dim3 grid((unsigned)np2m, (unsigned)((R + 31) / 32));
         kern<<<grid, 32 * nw, smem, st>>>(leaf_list, leaf.key.as<uint32_t>(),

@@ -14,11 +14,17 @@
 // CTA's points generated in shared memory (gen_row16). Tiles: m = 8 right-hand
 // sides, n = 8 nodes (P2M) or 8 points (L2P), k = 4 points (P2M) or 4 nodes (L2P).
 constexpr int kMRSpan = 64;                 // points per CTA pass
-constexpr int kMRRow = 52;                  // phase row stride (48 used)
+constexpr int kMRRow = 52;                  // L2P phase row stride (48 used; == 4 mod 8:
+                                            // points along g, nodes along tq)
+constexpr int kMRRowP = 50;                 // P2M phase row stride (== 2 mod 8: points along
+                                            // tq, nodes along g; 52 gave 2-way conflicts on
+                                            // every row read)
 constexpr int kMRNC = 32, kMRLS = 36;       // L2P node chunk, staged row stride (== 4 mod 8)
-constexpr int kMRLam = 40;                  // P2M staged weight row stride
+constexpr int kMRLam = 36;                  // P2M staged weight row stride (== 4 mod 16: the
+                                            // half-warp LDS.64 of (point tq, rhs g) is conflict-free)
 
-__device__ __forceinline__ void mr_gen_rows(double2 (*rows)[kMRRow], int t0, int np,
+template <int RS>
+__device__ __forceinline__ void mr_gen_rows(double2 (*rows)[RS], int t0, int np,
                                             const double* __restrict__ x0,
                                             const double* __restrict__ x1,
                                             const double* __restrict__ x2, const double c[3],
@@ -42,8 +48,8 @@ __global__ void __launch_bounds__(32 * NW, 384 / (32 * NW))
              double dxi, const int* __restrict__ node_m, const double* __restrict__ lam, int R,
              long long n, long long nleaf, double2* __restrict__ mult) {
   extern __shared__ __align__(16) double2 mr_dyn[];
-  double2 (*rows)[kMRRow] = reinterpret_cast<double2 (*)[kMRRow]>(mr_dyn);
-  double (*slam)[kMRLam] = reinterpret_cast<double (*)[kMRLam]>(mr_dyn + SPAN * kMRRow);
+  double2 (*rows)[kMRRowP] = reinterpret_cast<double2 (*)[kMRRowP]>(mr_dyn);
+  double (*slam)[kMRLam] = reinterpret_cast<double (*)[kMRLam]>(mr_dyn + SPAN * kMRRowP);
   const long long a = leaf_list ? leaf_list[blockIdx.x] : blockIdx.x;
   const int r0 = blockIdx.y * 32, rc = min(32, R - r0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -81,21 +87,41 @@ __global__ void __launch_bounds__(32 * NW, 384 / (32 * NW))
         mk[nt][1] = (v >> 8) & 255;
         mk[nt][2] = (v >> 16) & 255;
       }
-      for (int k0 = 0; k0 < np; k0 += 4) {
+      // the operands of k step k0 + 4 (weights, the two node phases: a chain
+      // of two complex products) are formed while the DMMAs of k step k0
+      // issue; formed inside the step they left the warp waiting on the DMUL /
+      // DFMA chain in front of every DMMA group (44 % of the stall samples)
+      double al[4], bq[2][2];
+      auto operands = [&](int k0) {
         const int j = k0 + tq;  // this lane's point (A column, B row)
-        double al[4];
 #pragma unroll
         for (int rt = 0; rt < 4; ++rt) al[rt] = slam[j][8 * rt + g];  // 0 past np
+        const double2* rw = rows[j < np ? j : 0];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const double2 q = cmul(cmul(rw[mk[nt][0]], rw[16 + mk[nt][1]]), rw[32 + mk[nt][2]]);
+          bq[nt][0] = q.x;
+          bq[nt][1] = -q.y;  // conj
+        }
+      };
+      operands(0);
+      for (int k0 = 0; k0 < np; k0 += 4) {
+        double ac[4], bc[2][2];
+#pragma unroll
+        for (int rt = 0; rt < 4; ++rt) ac[rt] = al[rt];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          bc[nt][0] = bq[nt][0];
+          bc[nt][1] = bq[nt][1];
+        }
+        if (k0 + 4 < np) operands(k0 + 4);
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           if (!tl[nt]) continue;
-          const double2* rw = rows[j < np ? j : 0];
-          const double2 q = cmul(cmul(rw[mk[nt][0]], rw[16 + mk[nt][1]]), rw[32 + mk[nt][2]]);
-          const double br = q.x, bi = -q.y;  // conj
 #pragma unroll
           for (int rt = 0; rt < 4; ++rt) {
-            dmma(vr[rt][nt][0], vr[rt][nt][1], al[rt], br);
-            dmma(vi[rt][nt][0], vi[rt][nt][1], al[rt], bi);
+            dmma(vr[rt][nt][0], vr[rt][nt][1], ac[rt], bc[nt][0]);
+            dmma(vi[rt][nt][0], vi[rt][nt][1], ac[rt], bc[nt][1]);
           }
         }
       }
