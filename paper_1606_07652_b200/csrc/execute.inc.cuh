@@ -26,6 +26,9 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
   }
   geo.L = L;
   const bool profiling = p->profiling && phase == 0;
+  // development builds: xp[3] = 1 records the stage events of the OVERLAPPED
+  // schedule (near field on its own stream, times.ms[5] = its fork-to-end time)
+  const bool serial_near = profiling && p->xp[3] != 1;
   // NVTX ranges name the stages' launch issue on the host timeline (nsys / ncu)
   static const char* const kStage[BLFMM_NSTAGES + 1] = {
       "blfmm gather", "blfmm p2m", "blfmm m2m", "blfmm m2l+l2l", "blfmm l2p", "blfmm near",
@@ -60,7 +63,7 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
       CK(cudaMemsetAsync(p->near_ctr.p, 0, sizeof(unsigned long long), sn));
       const long long ns = p->near_sym_min > 0 ? p->nsym : 0;
       // the serialised stage profile runs the near field alone at full occupancy
-      const unsigned gp = (unsigned)(p->num_sms * (p->profiling ? 5 : p->near_persist));
+      const unsigned gp = (unsigned)(p->num_sms * (serial_near ? 5 : p->near_persist));
       auto launchp = [&](auto kern) {
         kern<<<gp, 32 * kNearWarps, 0, sn>>>(
             p->near_ctr.as<unsigned long long>(), p->sym_work.as<int4>(),
@@ -130,10 +133,12 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
   }
   };
   auto fork_near = [&]() {
-    if (!profiling) {
+    if (!serial_near) {
       CK(cudaEventRecord(p->fork, st));
       CK(cudaStreamWaitEvent(p->stream_near, p->fork, 0));
+      if (profiling) CK(cudaEventRecord(p->ev_near[0], p->stream_near));
       launch_near(p->stream_near);
+      if (profiling) CK(cudaEventRecord(p->ev_near[1], p->stream_near));
       CK(cudaEventRecord(p->join, p->stream_near));
     }
   };
@@ -606,9 +611,9 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
     p->times.launches[4]++;
   }
   mark(5);
-  if (profiling) launch_near(st);  // serialised for per-stage timing
+  if (serial_near) launch_near(st);  // serialised for per-stage timing
   mark(6);
-  if (!profiling) CK(cudaStreamWaitEvent(st, p->join, 0));
+  if (!serial_near) CK(cudaStreamWaitEvent(st, p->join, 0));
   if (n) {
     if (p->world > 1 && !p->gather_sorted)  // non-owned entries are 0: a sum over ranks is u
       CK(cudaMemsetAsync(d_out, 0, sizeof(double) * R * n, st));
@@ -698,6 +703,12 @@ void collect_times(blfmm_plan* p) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]));
     p->times.ms[i] = ms;
+  }
+  if (p->xp[3] == 1) {
+    float ms = 0.f;
+    CK(cudaEventSynchronize(p->ev_near[1]));
+    CK(cudaEventElapsedTime(&ms, p->ev_near[0], p->ev_near[1]));
+    p->times.ms[5] = ms;
   }
 }
 

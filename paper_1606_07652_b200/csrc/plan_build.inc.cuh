@@ -762,6 +762,7 @@ void create_plan(const blfmm_plan_desc* desc, const blfmm_tuning* tune, blfmm_pl
   p->weight = d == 1 ? dxi : (d == 2 ? dxi * dxi : dxi * dxi * dxi);
   CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   for (auto& e : p->ev) CK(cudaEventCreate(&e));
+  for (auto& e : p->ev_near) CK(cudaEventCreate(&e));
   CK(cudaEventCreateWithFlags(&p->fence_in, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&p->fence_out, cudaEventDisableTiming));
   {

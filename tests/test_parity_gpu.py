@@ -716,8 +716,10 @@ def test_half_spectrum_general_even_m(blfmm, oracle, spec, m, n, leaf):
         assert np.linalg.norm(eh - ef) <= 1e-12 * np.linalg.norm(ef)
 
 
-@pytest.mark.parametrize("spec,m,n,leaf", [("imq:c=0.1", 20, 6000, 2), ("gaussian:c=64", 58, 3000, 2)])
-def test_half_spectrum_stats_free_3m_kernels(blfmm, oracle, spec, m, n, leaf):
+@pytest.mark.parametrize("spec,m,n,leaf,nrhs", [("imq:c=0.1", 20, 6000, 2, 1),
+                                                ("gaussian:c=64", 58, 3000, 2, 1),
+                                                ("mq:c=0.2", 24, 5000, 2, 3)])
+def test_half_spectrum_stats_free_3m_kernels(blfmm, oracle, spec, m, n, leaf, nrhs):
     """The stats-free matvec of the general half spectrum (what a Krylov loop
     and the bench time) runs block A on the 3-multiplication DMMA kernels
     (k_p2m_big3: B staged once per leaf group, chunks of 96 points;
@@ -728,22 +730,27 @@ def test_half_spectrum_stats_free_3m_kernels(blfmm, oracle, spec, m, n, leaf):
     import torch
     W = I.WORKLOADS["P3"]
     x, w = W.make(n)
+    if nrhs > 1:  # several right-hand sides: grid.z of the same kernels
+        w = np.stack([np.roll(w, 17 * r) * (1.0 + 0.25 * r) for r in range(nrhs)])
     sigma = math.pi
     res, plan = gpu_mlfmm(blfmm, x, w, spec, sigma, m, leaf)
     k = plan.kernels()
     assert k["p2m"] == "k_p2m_big3+k_p2m_axes" and k["l2p"] == "k_l2p_axes+k_l2p_half_a3", k
-    lam = torch.from_numpy(np.ascontiguousarray(w.reshape(1, -1))).cuda()
+    lam = torch.from_numpy(np.ascontiguousarray(w.reshape(nrhs, -1))).cuda()
     out = torch.empty_like(lam)
+    ref = np.asarray(res.values).reshape(nrhs, -1)
     for _ in range(2):  # direct launch, then the captured graph
         out.zero_()
         assert plan.execute_device(lam.data_ptr(), out.data_ptr(), stats=False) is None
         torch.cuda.synchronize()
-        u = out.cpu().numpy()[0]
-        assert rel_l2(u, res.values) <= 1e-13, rel_l2(u, res.values)
+        u = out.cpu().numpy()
+        assert rel_l2(u, ref) <= 1e-13, rel_l2(u, ref)
     ctab = blfmm.translation_coefficients(blfmm.parse_kernel_spec(spec),
                                           blfmm.make_quadrature(sigma, m, 3)).c_vals
     ov, _, _ = oracle.mlfmm(x, w, spec, sigma, m, leaf, c_table_in=ctab)
-    assert rel_l2(u, ov) <= TOL, rel_l2(u, ov)
+    ov = np.asarray(ov).reshape(nrhs, -1)
+    for r in range(nrhs):
+        assert rel_l2(u[r], ov[r]) <= TOL, (r, rel_l2(u[r], ov[r]))
 
 
 def test_half_spectrum_general_even_m_batched(blfmm, oracle):
