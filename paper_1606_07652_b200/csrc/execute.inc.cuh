@@ -542,11 +542,10 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
                                     leaf.loc.as<double2>(), R, n, leaf.nbox, p->weight,
                                     p->far_.as<double>(), p->imag_bits.as<unsigned long long>());
     } else if (D == 3 && p->herm && !p->h16) {
-      dim3 gr((unsigned)p->nwork8, 1, R);
-      k_l2p_axes<<<gr, 128, 0, st>>>(p->work8.as<int2>(), p->leaf_start.as<int>(),
-                                     p->pht.as<double2>(), leaf.loc.as<double2>(), M, K, n,
-                                     leaf.nbox, p->weight, p->far_.as<double>(),
-                                     p->himag.as<double>());
+      k_l2p_axes<1><<<dim3((unsigned)p->nwork8, 1, R), 128, 0, st>>>(
+          p->work8.as<int2>(), p->leaf_start.as<int>(), p->pht.as<double2>(),
+          leaf.loc.as<double2>(), M, K, n, leaf.nbox, p->weight, p->far_.as<double>(),
+          p->himag.as<double>());
       // block A: 32 points per CTA (16 with the imaginary-residual GEMM)
       auto la = [&](auto kern, const DevBuf& wk, long long nw) {
         kern<<<dim3((unsigned)nw, 1, R), 128, 0, st>>>(
@@ -589,15 +588,14 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
                                         p->dtab.as<double>(), n, leaf.nbox, p->weight,
                                         p->far_.as<double>(), p->imag_bits.as<unsigned long long>());
     } else if (D == 2 && p->g2d16) {
-      const bool s32 = p->xp[0] == 1;
-      const long long nw = s32 ? p->nwork32 : p->nwork128;
-      dim3 grid((unsigned)((nw + 3) / 4), 1, R);
-      k_l2p_2d16<<<grid, 128, 0, st>>>((s32 ? p->work32 : p->work128).as<int2>(), nw,
+      // warp items of 128-point spans (k_l2p_2d16's header)
+      dim3 grid((unsigned)((p->nwork128 + 3) / 4), 1, R);
+      k_l2p_2d16<<<grid, 128, 0, st>>>(p->work128.as<int2>(), p->nwork128,
                                        leaf.key.as<uint32_t>(), p->leaf_start.as<int>(), x0, x1,
                                        leaf.loc.as<double2>(), n, leaf.nbox, L, p->lo[0], p->lo[1],
                                        side[0], side[1], p->sigma, 2.0 * p->sigma / M, p->weight,
                                        p->far_.as<double>(),
-                                       p->imag_bits.as<unsigned long long>(), s32 ? 32 : kL2PSpan);
+                                       p->imag_bits.as<unsigned long long>(), kL2PSpan);
     } else {
       constexpr int WN = 4;
       dim3 grid((unsigned)p->nwork8, 1, R);

@@ -86,65 +86,93 @@ __global__ void __launch_bounds__(256, 1)
     }
 }
 
-// L2P of blocks C / B1 / B2 for an 8-point tile (work8): for each block
-// W_i[a] = sum_b Pb_i[b] L[a][b] on DMMA (A = the points' Pb, B = L^T; warp w
-// takes row tiles w and w + 4), then part_i += Pf_i[f0] sum_a Pa_i[a] W_i[a].
-// Writes far_[i] = w Re part_i and imag_acc[i] = w Im part_i (block A adds to
-// both afterwards, k_l2p_half_a).
+// L2P of blocks C / B1 / B2 for PT 8-point tiles of one leaf (work8: PT = 1):
+// for each block W_i[a] = sum_b Pb_i[b] L[a][b] on DMMA (A = the points' Pb,
+// B = L^T, each B fragment loaded one k step ahead of its use; warp w takes row
+// tiles w and w + 4), then part_i += Pf_i[f0] sum_a Pa_i[a] W_i[a]. Writes
+// far_[i] = w Re part_i and imag_acc[i] = w Im part_i (block A adds to both
+// afterwards). (PT = 4 on 32-point items measured the same as PT = 1: 10.04 vs
+// 10.02 ms of P2 L2P; the same prefetch of k_p2m_axes' A fragment was slower,
+// 7.75 -> 8.35 ms.)
+template <int PT>
 __global__ void __launch_bounds__(128)
     k_l2p_axes(const int2* __restrict__ work, const int* __restrict__ leaf_start,
                const double2* __restrict__ pht, const double2* __restrict__ loc, int M,
                long long K, long long n, long long nleaf, double weight,
                double* __restrict__ far_, double* __restrict__ imag_acc) {
-  __shared__ double2 red[4][8];
+  __shared__ double2 red[4][8 * PT];
   const int2 item = work[blockIdx.x];
   const long long lf = item.x;
   const int r = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tq = lane & 3;
-  const int p1 = leaf_start[lf + 1], pb = item.y;
+  const int pb = item.y, p1 = min(leaf_start[lf + 1], pb + 8 * PT);
   const int per = 3 * M;
-  const int ia = pb + g;  // A row / C row: point
-  const bool iv = ia < p1;
-  const double2* pi = pht + (long long)(iv ? ia : pb) * per;
+  const double2 zero = make_double2(0.0, 0.0);
+  const double2* pi[PT];  // A row / C row: point 8 pt + g
+  bool iv[PT];
+#pragma unroll
+  for (int pt = 0; pt < PT; ++pt) {
+    const int ia = pb + 8 * pt + g;
+    iv[pt] = ia < p1;
+    pi[pt] = pht + (long long)(iv[pt] ? ia : pb) * per;
+  }
   const double2* la = loc + ((long long)r * nleaf + lf) * K;
-  double2 part = make_double2(0.0, 0.0);
+  double2 part[PT];
+#pragma unroll
+  for (int pt = 0; pt < PT; ++pt) part[pt] = zero;
   for (int blk = 0; blk < 3; ++blk) {
     const HalfAxes hb = half_block(blk, M);
-    const double2 pf = __ldg(pi + hb.fx * M + hb.f0);
-    double2 bpart = make_double2(0.0, 0.0);
+    double2 bpart[PT];
+#pragma unroll
+    for (int pt = 0; pt < PT; ++pt) bpart[pt] = zero;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int rt = warp + 4 * q;  // row tile of a
       if (8 * rt >= hb.na) continue;
       const int arow = 8 * rt + g;  // B column n = g: row a of L
       const bool av = arow < hb.na;
-      CTile acc = CTile{{0.0, 0.0}, {0.0, 0.0}};
+      const double2* lrow = la + hb.off + (long long)(av ? arow : 0) * hb.stride;
+      CTile acc[PT];
+#pragma unroll
+      for (int pt = 0; pt < PT; ++pt) acc[pt] = CTile{{0.0, 0.0}, {0.0, 0.0}};
+      double2 lv = (av && tq < hb.nb) ? __ldg(lrow + tq) : zero;
       for (int k0 = 0; k0 < hb.nb; k0 += 4) {
         const int c = k0 + tq;
         const bool cv = c < hb.nb;
-        const double2 z = (iv && cv) ? __ldg(pi + hb.bx * M + hb.b0 + c) : make_double2(0.0, 0.0);
-        const double2 lv = (av && cv) ? __ldg(la + hb.off + (long long)arow * hb.stride + c)
-                                      : make_double2(0.0, 0.0);
-        cdmma(acc, z.x, z.y, -z.y, lv.x, lv.y);
+        const double2 lc = lv;
+        lv = (av && c + 4 < hb.nb) ? __ldg(lrow + c + 4) : zero;
+#pragma unroll
+        for (int pt = 0; pt < PT; ++pt) {
+          const double2 z = (iv[pt] && cv) ? __ldg(pi[pt] + hb.bx * M + hb.b0 + c) : zero;
+          cdmma(acc[pt], z.x, z.y, -z.y, lc.x, lc.y);
+        }
       }
       // C[point g][a = 8 rt + 2 tq + v]
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int aa = 8 * rt + 2 * tq + v;
-        if (aa >= hb.na || !iv) continue;
-        cmac(bpart, __ldg(pi + hb.ax * M + hb.a0 + aa), make_double2(acc.re[v], acc.im[v]));
+        if (aa >= hb.na) continue;
+#pragma unroll
+        for (int pt = 0; pt < PT; ++pt)
+          if (iv[pt])
+            cmac(bpart[pt], __ldg(pi[pt] + hb.ax * M + hb.a0 + aa),
+                 make_double2(acc[pt].re[v], acc[pt].im[v]));
       }
     }
-    cmac(part, pf, bpart);
+#pragma unroll
+    for (int pt = 0; pt < PT; ++pt) cmac(part[pt], __ldg(pi[pt] + hb.fx * M + hb.f0), bpart[pt]);
   }
-  for (int off = 1; off < 4; off <<= 1) {
-    part.x += __shfl_xor_sync(0xffffffffu, part.x, off);
-    part.y += __shfl_xor_sync(0xffffffffu, part.y, off);
+#pragma unroll
+  for (int pt = 0; pt < PT; ++pt) {
+    for (int off = 1; off < 4; off <<= 1) {
+      part[pt].x += __shfl_xor_sync(0xffffffffu, part[pt].x, off);
+      part[pt].y += __shfl_xor_sync(0xffffffffu, part[pt].y, off);
+    }
+    if (tq == 0) red[warp][8 * pt + g] = part[pt];
   }
-  if (tq == 0) red[warp][g] = part;
   __syncthreads();
-  if (threadIdx.x < 8 && pb + threadIdx.x < p1) {
+  if (threadIdx.x < 8 * PT && pb + threadIdx.x < p1) {
     double2 sum = red[0][threadIdx.x];
     for (int w = 1; w < 4; ++w) {
       sum.x += red[w][threadIdx.x].x;
