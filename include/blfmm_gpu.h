@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define BLFMM_GPU_ABI_VERSION 3
+#define BLFMM_GPU_ABI_VERSION 4
 
 /* Status codes (reference exception class in parentheses). */
 enum blfmm_status {
@@ -52,18 +52,21 @@ enum blfmm_status {
   BLFMM_EACCURACY = 3, /* blfmm::accuracy_error; see blfmm_last_error_value */
   BLFMM_ECUDA = 4,     /* CUDA runtime error, or no usable device     */
   BLFMM_ENCCL = 5,     /* multi-GPU exchange error                    */
-  BLFMM_ENOMEM = 6     /* device allocation failed                    */
+  BLFMM_ENOMEM = 6,    /* device allocation failed                    */
+  BLFMM_ELENGTH = 7    /* std::length_error (dense backend, N > 8192) */
 };
 
-/* RadialKernel::type (kernels.hpp:12-17); only the band-limited FMM kernels
- * of the north star are executable on the GPU path. */
+/* RadialKernel::type (kernels.hpp:12-17). The band-limited FMM plan takes the
+ * north star's three kernels; the O(N^2) sum (blfmm_direct) and the dense
+ * Krylov backend (blfmm_solve_dense) evaluate every type (eval_kernel,
+ * kernels.cpp:131-161). */
 enum blfmm_kernel_type {
   BLFMM_KERNEL_GAUSSIAN = 0, /* phi = exp(-c r^2)      */
   BLFMM_KERNEL_MQ = 1,       /* phi = sqrt(r^2 + c^2)  */
   BLFMM_KERNEL_IMQ = 2,      /* phi = 1/sqrt(r^2+c^2)  */
-  BLFMM_KERNEL_TPS = 3,      /* parsed, EDOMAIN on the GPU path */
-  BLFMM_KERNEL_WENDLAND_C2 = 4,
-  BLFMM_KERNEL_WENDLAND31 = 5
+  BLFMM_KERNEL_TPS = 3,         /* phi = (-1)^{1+beta/2} r^beta log r; EDOMAIN for a plan */
+  BLFMM_KERNEL_WENDLAND_C2 = 4, /* phi = (1 - eps r)_+^4 (4 eps r + 1); EDOMAIN for a plan */
+  BLFMM_KERNEL_WENDLAND31 = 5   /* phi = (1 - eps r)_+^3 (3 eps r + 1); EDOMAIN for a plan */
 };
 
 /* GridMode (mlfmm.hpp:21-28). `scaled` (per-level halved band, Lagrange
@@ -290,6 +293,15 @@ typedef struct blfmm_solve_stats {
 } blfmm_solve_stats;
 int blfmm_solve(blfmm_plan* plan, int method, const double* b, double* x, double tol,
                 int max_iter, blfmm_solve_stats* stats);
+
+/* solve_interpolation's Backend::dense (solver.cpp:207-262, 269-275): the same
+ * Krylov loops on the dense kernel matrix A_ij = phi(|x_i - x_j|), applied
+ * matrix-free on the device (the O(N^2) kernel of blfmm_direct) instead of
+ * assembled with Eigen. coords: HOST [n][d]; every RadialKernel type. N > 8192
+ * returns BLFMM_ELENGTH (assemble_dense's std::length_error). */
+int blfmm_solve_dense(int d, long long n, const double* coords, int kernel_type, double shape,
+                      int method, const double* b, double* x, double tol, int max_iter,
+                      blfmm_solve_stats* stats, int device);
 
 /* Independent O(N^2) check (direct_matvec, fmm.cpp:30-75): values for
  * n_targets target indices (NULL = all n) into HOST out. */

@@ -48,6 +48,8 @@ inline void check(int code) {
       throw accuracy_error(msg, blfmm_last_error_value());
     case BLFMM_ENOMEM:
       throw std::bad_alloc();
+    case BLFMM_ELENGTH:
+      throw std::length_error(msg);
     default:
       throw std::runtime_error("blfmm_gpu: " + msg);
   }
@@ -236,7 +238,9 @@ inline SumResult direct_matvec(const RadialKernel& k, const PointSet& ps,
 // (Backend::single_fmm, lround(log2(sqrt N)) >= 2; shared grids make the
 // multilevel sweep equal to the single-level sum to rounding). CG for the
 // positive definite kernels (kernels.cpp:334-337), restarted GMRES otherwise.
-// Backend::dense needs the reference's Eigen assembly and is refused.
+// Backend::dense (the reference's default; Eigen assembly + a * x there) runs
+// the same loops on the matrix-free O(N^2) device kernel (blfmm_solve_dense),
+// for every kernel type, N <= 8192 (std::length_error beyond, as assemble_dense).
 enum class Backend { dense, single_fmm, mlfmm };
 struct InterpolationProblem {
   RadialKernel kernel;
@@ -265,8 +269,31 @@ inline std::pair<std::vector<double>, SolveStats> solve_interpolation(
   if (prob.rhs.size() != static_cast<std::size_t>(n))
     throw std::invalid_argument("rhs length != point count");
   if (!(prob.tol > 0.0)) throw std::invalid_argument("tol must be positive");
-  if (prob.backend == Backend::dense)
-    throw std::domain_error("dense backend needs the reference's Eigen assembly");
+  // positive_definite, kernels.cpp:334-337
+  const bool pd = prob.kernel.type == KernelType::Gaussian || prob.kernel.type == KernelType::IMQ ||
+                  prob.kernel.type == KernelType::WendlandC2 ||
+                  prob.kernel.type == KernelType::Wendland31;
+  auto finish = [&](int rc, const blfmm_solve_stats& st, std::vector<double>& x) {
+    SolveStats out;
+    out.iterations = st.iterations;
+    out.residual = st.residual;
+    out.matvecs = st.matvecs;
+    out.method = st.method == BLFMM_SOLVE_CG ? "cg" : "gmres";
+    out.converged = st.converged != 0;
+    check(rc);  // BLFMM_EACCURACY -> accuracy_error (best residual), as the reference
+    return std::pair<std::vector<double>, SolveStats>{std::move(x), out};
+  };
+  if (prob.backend == Backend::dense) {
+    std::vector<double> coords(static_cast<std::size_t>(n) * ps.d);
+    for (int i = 0; i < n; ++i)
+      for (int q = 0; q < ps.d; ++q) coords[static_cast<std::size_t>(i) * ps.d + q] = ps.pts[i][q];
+    std::vector<double> x(n, 0.0);
+    blfmm_solve_stats st{};
+    const int rc = blfmm_solve_dense(ps.d, n, coords.data(), static_cast<int>(prob.kernel.type),
+                                     prob.kernel.shape, pd ? BLFMM_SOLVE_CG : BLFMM_SOLVE_GMRES,
+                                     prob.rhs.data(), x.data(), prob.tol, prob.max_iter, &st, -1);
+    return finish(rc, st, x);
+  }
   const double sigma = prob.sigma > 0.0 ? prob.sigma : 3.14159265358979323846;
   const int m = prob.m_per_dim > 0 ? prob.m_per_dim : choose_truncation(n);
   int level;
@@ -280,19 +307,11 @@ inline std::pair<std::vector<double>, SolveStats> solve_interpolation(
   BoxTree tree = build_tree(ps, level);
   LevelGrids grids = make_level_grids(prob.kernel, sigma, m, ps.d, level, GridMode::shared, 10);
   blfmm_plan* p = plan_for(ps, tree, prob.kernel, sigma, m, grids.factors[level].c_vals);
-  const bool pd = prob.kernel.type == KernelType::Gaussian || prob.kernel.type == KernelType::IMQ;
   std::vector<double> x(n, 0.0);
   blfmm_solve_stats st{};
   const int rc = blfmm_solve(p, pd ? BLFMM_SOLVE_CG : BLFMM_SOLVE_GMRES, prob.rhs.data(),
                              x.data(), prob.tol, prob.max_iter, &st);
-  SolveStats out;
-  out.iterations = st.iterations;
-  out.residual = st.residual;
-  out.matvecs = st.matvecs;
-  out.method = st.method == BLFMM_SOLVE_CG ? "cg" : "gmres";
-  out.converged = st.converged != 0;
-  check(rc);  // BLFMM_EACCURACY -> accuracy_error (best residual), as the reference
-  return {std::move(x), out};
+  return finish(rc, st, x);
 }
 
 }  // namespace gpu

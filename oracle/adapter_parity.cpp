@@ -143,8 +143,73 @@ static int solve_case(const char* name, const std::string& spec, int n, double s
   return ok ? 0 : 1;
 }
 
+// Backend::dense through the adapter (blfmm_solve_dense: the Krylov loop on the
+// matrix-free O(N^2) device kernel): the solution's residual under the matrix
+// assembled with the REFERENCE's eval_kernel / dist exactly as assemble_dense
+// (solver.cpp:207-240), the method the reference picks (positive_definite),
+// and the N <= 8192 cap as std::length_error.
+static int dense_case(const std::string& spec, int d, int n, const char* method) {
+  PointSet ps;
+  ps.d = d;
+  for (int i = 0; i < n; ++i) {
+    if (d == 1) ps.pts.push_back(Pt{(i + 0.5 + 0.3 * (uniform01(3101, i) - 0.5)) / n, 0.0});
+    else ps.pts.push_back(Pt{uniform01(3102, 2 * i), uniform01(3102, 2 * i + 1)});
+  }
+  std::vector<double> b(n);
+  for (int j = 0; j < n; ++j) b[j] = std::sin(M_PI * ps.pts[j][0]) + 0.25 * std::cos(2.0 * ps.pts[j][1]);
+  RadialKernel k = parse_kernel_spec(spec);
+  blfmm::gpu::InterpolationProblem prob;
+  prob.kernel = k;
+  prob.ps = &ps;
+  prob.rhs = b;
+  prob.backend = blfmm::gpu::Backend::dense;
+  prob.tol = 1e-9;
+  prob.max_iter = 4000;
+  std::vector<double> x;
+  blfmm::gpu::SolveStats st;
+  try {
+    std::tie(x, st) = blfmm::gpu::solve_interpolation(prob);
+  } catch (const std::exception& e) {
+    std::printf("{\"case\": \"dense %s\", \"error\": \"%s\", \"ok\": false}\n", spec.c_str(),
+                e.what());
+    return 1;
+  }
+  double res = 0, bn = 0;
+  for (int i = 0; i < n; ++i) {
+    double acc = 0;
+    for (int j = 0; j < n; ++j) acc += eval_kernel(k, dist(d, ps.pts[i], ps.pts[j])) * x[j];
+    res += (acc - b[i]) * (acc - b[i]);
+    bn += b[i] * b[i];
+  }
+  res = std::sqrt(res / bn);
+  const bool ok = st.converged && st.method == method && res <= 20 * prob.tol;
+  std::printf("{\"case\": \"dense %s d=%d N=%d\", \"method\": \"%s\", \"iterations\": %d, "
+              "\"residual_ref_matrix\": %.3e, \"ok\": %s}\n",
+              spec.c_str(), d, n, st.method.c_str(), st.iterations, res, ok ? "true" : "false");
+  return ok ? 0 : 1;
+}
+
 int main() {
   int fails = 0;
+  fails += dense_case("tps:beta=2", 1, 200, "gmres");  // test_solver.cpp:286-303's kernel
+  fails += dense_case("wendland:eps=4", 2, 400, "cg");
+  fails += dense_case("imq:c=0.01", 1, 200, "cg");
+  fails += dense_case("mq:c=0.05", 2, 300, "gmres");
+  try {  // assemble_dense's cap (solver.cpp:211)
+    PointSet big;
+    big.d = 1;
+    for (int i = 0; i < 8193; ++i) big.pts.push_back(Pt{i / 8193.0, 0.0});
+    blfmm::gpu::InterpolationProblem prob;
+    prob.kernel = parse_kernel_spec("gaussian:c=1");
+    prob.ps = &big;
+    prob.rhs.assign(8193, 1.0);
+    prob.backend = blfmm::gpu::Backend::dense;
+    blfmm::gpu::solve_interpolation(prob);
+    std::printf("{\"case\": \"dense cap\", \"ok\": false}\n");
+    ++fails;
+  } catch (const std::length_error&) {
+    std::printf("{\"case\": \"dense cap\", \"ok\": true}\n");
+  }
   fails += solve_case("gaussian:c=256 band-capturing 1D N=512", "gaussian:c=256", 512, 203.0,
                       2112, 4);
   fails += solve_case("gaussian:c=256 band-capturing 1D N=1024", "gaussian:c=256", 1024, 203.0,

@@ -40,7 +40,7 @@ constexpr double kPi = 3.14159265358979323846;
 constexpr double kTwoPi = 2.0 * kPi;
 constexpr double kPoleBall = 1e-8;  // bandlimit.cpp:20
 
-enum KType { GAUSSIAN = 0, MQ = 1, IMQ = 2 };
+enum KType { GAUSSIAN = 0, MQ = 1, IMQ = 2, TPS = 3, WENDLAND_C2 = 4, WENDLAND31 = 5 };
 
 struct Kernel {
   int type;
@@ -69,6 +69,26 @@ double eval_kernel(const Kernel& k, double r) {
       return std::sqrt(r * r + c * c);
     case IMQ:
       return 1.0 / std::sqrt(r * r + c * c);
+    case TPS: {  // kernels.cpp:141-146: sign r^beta log r, 0 at r = 0
+      if (r == 0.0) return 0.0;
+      int beta = static_cast<int>(c);
+      double sign = (1 + beta / 2) % 2 == 0 ? 1.0 : -1.0;
+      double p = 1.0;  // pow_int: repeated multiplication
+      for (int q = 0; q < beta; ++q) p *= r;
+      return sign * p * std::log(r);
+    }
+    case WENDLAND_C2: {  // kernels.cpp:147-152
+      double u = c * r;
+      if (u >= 1.0) return 0.0;
+      double v = 1.0 - u;
+      return v * v * v * v * (4.0 * u + 1.0);
+    }
+    case WENDLAND31: {  // kernels.cpp:153-158
+      double u = c * r;
+      if (u >= 1.0) return 0.0;
+      double v = 1.0 - u;
+      return v * v * v * (3.0 * u + 1.0);
+    }
   }
   throw std::domain_error("unsupported kernel type");
 }

@@ -18,7 +18,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _ORC = os.path.join(HERE, "liboracle.so")
 _REF = os.path.join(HERE, "_ref", "libblfmm_ref.so")
 
-KTYPES = {"gaussian": 0, "ga": 0, "mq": 1, "multiquadric": 1, "imq": 2}
+KTYPES = {"gaussian": 0, "ga": 0, "mq": 1, "multiquadric": 1, "imq": 2, "tps": 3,
+          "wendland": 4, "wendlandc2": 4, "wendland31": 5}
+_DEFAULT_SHAPE = {3: 2.0, 4: 0.5, 5: 0.5}  # parse_kernel_spec defaults (kernels.cpp)
 
 _dp = ct.POINTER(ct.c_double)
 _lp = ct.POINTER(ct.c_longlong)
@@ -77,7 +79,7 @@ def _chk(code, which="orc"):
 
 def parse_spec(spec: str):
     name, _, param = spec.lower().partition(":")
-    shape = 1.0
+    shape = _DEFAULT_SHAPE.get(KTYPES[name], 1.0)
     if param:
         shape = float(param.split("=", 1)[1])
     return KTYPES[name], shape

@@ -7,7 +7,7 @@ reference library's interface (see ``api``) plus the seeded input generators
 """
 from .api import *  # noqa: F401,F403
 from .api import (AccuracyError, BlfmmError, BoundingBox, BoxTree, CudaError,  # noqa: F401
-                  DomainError, GridMode, InvalidArgument, KernelType, LevelGrids,
+                  DomainError, GridMode, InvalidArgument, KernelType, LengthError, LevelGrids,
                   LowRankFactors, Plan, PointSet, QuadratureGrid, RadialKernel, SumRequest,
                   SumResult, SumStats, bandlimited_radial_table, build_tree, choose_truncation,
                   couple, direct_matvec, direct_matvec_hybrid, eval_bandlimited,

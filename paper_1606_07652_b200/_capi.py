@@ -11,7 +11,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libblfmm_gpu.so")
 
-OK, EINVAL, EDOMAIN, EACCURACY, ECUDA, ENCCL, ENOMEM = range(7)
+OK, EINVAL, EDOMAIN, EACCURACY, ECUDA, ENCCL, ENOMEM, ELENGTH = range(8)
 NSTAGES = 7
 STAGE_NAMES = ("gather", "p2m", "m2m", "m2l_l2l", "l2p", "near", "combine")
 
@@ -127,6 +127,10 @@ EXPORTS = {
     "blfmm_solve": (ct.c_int, [ct.c_void_p, ct.c_int, ct.POINTER(ct.c_double),
                                ct.POINTER(ct.c_double), ct.c_double, ct.c_int,
                                ct.POINTER(SolveStatsC)]),
+    "blfmm_solve_dense": (ct.c_int, [ct.c_int, ct.c_longlong, ct.POINTER(ct.c_double), ct.c_int,
+                                     ct.c_double, ct.c_int, ct.POINTER(ct.c_double),
+                                     ct.POINTER(ct.c_double), ct.c_double, ct.c_int,
+                                     ct.POINTER(SolveStatsC), ct.c_int]),
     "blfmm_plan_attach_nccl": (ct.c_int, [ct.c_void_p, ct.c_char_p]),
     "blfmm_plan_attach_comm": (ct.c_int, [ct.c_void_p, ct.POINTER(CommOps)]),
     "blfmm_direct": (ct.c_int, [ct.c_int, ct.c_longlong, ct.POINTER(ct.c_double), ct.c_int,
@@ -173,6 +177,10 @@ class DomainError(BlfmmError, ArithmeticError):
     """std::domain_error"""
 
 
+class LengthError(BlfmmError, ValueError):
+    """std::length_error (assemble_dense's N <= 8192 cap, solver.cpp:211)"""
+
+
 class AccuracyError(BlfmmError):
     """blfmm::accuracy_error (common.hpp:33-41)"""
 
@@ -198,4 +206,6 @@ def check(code: int):
         raise AccuracyError(msg, l.blfmm_last_error_value())
     if code == ENOMEM:
         raise MemoryError(msg)
+    if code == ELENGTH:
+        raise LengthError(msg)
     raise CudaError(f"[{code}] {msg}")

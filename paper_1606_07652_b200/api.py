@@ -32,7 +32,7 @@ import numpy as np
 
 from . import _capi
 from ._capi import (AccuracyError, BlfmmError, CudaError, DomainError,  # noqa: F401
-                    InvalidArgument)
+                    InvalidArgument, LengthError)
 
 _dp = ct.POINTER(ct.c_double)
 

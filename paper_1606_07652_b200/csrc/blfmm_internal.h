@@ -26,6 +26,10 @@ KernelSpec parse_spec(const std::string& spec);
 void set_error(const Error& e);
 void set_error_message(const char* msg);
 void require_fmm_kernel(const KernelSpec& k);
+void require_radial_kernel(const KernelSpec& k);  // any RadialKernel::type with a valid shape
+// dense kernel matvec on device vectors (blfmm.cu), the operator of blfmm_solve_dense
+void direct_device(int d, long long n, const double* d_x, int type, double shape,
+                   const double* d_in, double* d_out, void* stream);
 double fourier_value(const KernelSpec& k, double xi, int d);
 std::vector<double> translation_spectrum(const KernelSpec& k, double sigma,
                                          int m, int d);

@@ -10,6 +10,23 @@ __device__ __forceinline__ double phi_ref(int type, double c, double r) {
   r = fabs(r);
   const double rr = __dmul_rn(r, r);
   if (type == BLFMM_KERNEL_GAUSSIAN) return exp(__dmul_rn(__dmul_rn(-c, r), r));
+  if (type == BLFMM_KERNEL_TPS) {  // kernels.cpp:141-146: sign r^beta log r, 0 at r = 0
+    if (r == 0.0) return 0.0;
+    const int beta = static_cast<int>(c);
+    double p = 1.0;  // pow_int: repeated multiplication
+    for (int q = 0; q < beta; ++q) p = __dmul_rn(p, r);
+    const double sign = (1 + beta / 2) % 2 == 0 ? 1.0 : -1.0;
+    return __dmul_rn(__dmul_rn(sign, p), log(r));
+  }
+  if (type == BLFMM_KERNEL_WENDLAND_C2 || type == BLFMM_KERNEL_WENDLAND31) {
+    const double u = __dmul_rn(c, r);  // kernels.cpp:147-158
+    if (u >= 1.0) return 0.0;
+    const double v = __dadd_rn(1.0, -u);
+    const double v3 = __dmul_rn(__dmul_rn(v, v), v);
+    if (type == BLFMM_KERNEL_WENDLAND_C2)
+      return __dmul_rn(__dmul_rn(v3, v), __dadd_rn(__dmul_rn(4.0, u), 1.0));
+    return __dmul_rn(v3, __dadd_rn(__dmul_rn(3.0, u), 1.0));
+  }
   const double q = __dsqrt_rn(__dadd_rn(rr, __dmul_rn(c, c)));
   return type == BLFMM_KERNEL_IMQ ? __ddiv_rn(1.0, q) : q;
 }

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <limits>
 #include <string>
@@ -115,7 +116,11 @@ struct Vecs {
 };
 
 // solver.cpp:43-88
-void run_cg(blfmm_plan* plan, Vecs& v, const double* b, double* x, double tol, int max_iter,
+// y = A x on device vectors, on the solve's stream: the plan's FMM matvec
+// (blfmm_solve) or the dense kernel sum (blfmm_solve_dense)
+using Apply = std::function<void(const double*, double*)>;
+
+void run_cg(const Apply& apply, Vecs& v, const double* b, double* x, double tol, int max_iter,
             blfmm_solve_stats& st) {
   const long long n = v.n;
   st.method = BLFMM_SOLVE_CG;
@@ -133,7 +138,7 @@ void run_cg(blfmm_plan* plan, Vecs& v, const double* b, double* x, double tol, i
   double rr = v.dot(r, r);
   double best = std::sqrt(rr) / bnorm;
   for (int it = 0; it < max_iter; ++it) {
-    ckb(blfmm_execute_device(plan, p, ap, nullptr, v.st));
+    apply(p, ap);
     ++st.matvecs;
     const double pap = v.dot(p, ap);
     if (pap <= 0.0) break;  // matrix not PD to working precision
@@ -161,7 +166,7 @@ void run_cg(blfmm_plan* plan, Vecs& v, const double* b, double* x, double tol, i
 
 // solver.cpp:90-203 (restart min(max_iter, 300), modified Gram-Schmidt,
 // Givens rotations, breakdown at |w| < 1e-14 beta)
-void run_gmres(blfmm_plan* plan, Vecs& v, const double* b, double* x, double tol, int max_iter,
+void run_gmres(const Apply& apply, Vecs& v, const double* b, double* x, double tol, int max_iter,
                blfmm_solve_stats& st) {
   const long long n = v.n;
   st.method = BLFMM_SOLVE_GMRES;
@@ -181,7 +186,7 @@ void run_gmres(blfmm_plan* plan, Vecs& v, const double* b, double* x, double tol
     if (total_it == 0) {
       ck(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, v.st));
     } else {
-      ckb(blfmm_execute_device(plan, x, r, nullptr, v.st));
+      apply(x, r);
       ++st.matvecs;
       v.bminus(r, b);
     }
@@ -198,7 +203,7 @@ void run_gmres(blfmm_plan* plan, Vecs& v, const double* b, double* x, double tol
     std::vector<double> cs, sn, g{beta};
     int k = 0;
     for (; k < m; ++k) {
-      ckb(blfmm_execute_device(plan, basis[k], w, nullptr, v.st));
+      apply(basis[k], w);
       ++st.matvecs;
       h.emplace_back(k + 2, 0.0);
       for (int j = 0; j <= k; ++j) {
@@ -241,7 +246,7 @@ void run_gmres(blfmm_plan* plan, Vecs& v, const double* b, double* x, double tol
       y[j] = s / h[j][j];
     }
     for (int j = 0; j < k; ++j) v.axpy(x, basis[j], y[j]);
-    ckb(blfmm_execute_device(plan, x, r, nullptr, v.st));
+    apply(x, r);
     ++st.matvecs;
     v.bminus(r, b);
     const double res = std::sqrt(v.dot(r, r)) / bnorm;
@@ -261,17 +266,16 @@ void run_gmres(blfmm_plan* plan, Vecs& v, const double* b, double* x, double tol
 }  // namespace
 }  // namespace blfmm_gpu
 
-extern "C" int blfmm_solve(blfmm_plan* plan, int method, const double* b, double* x, double tol,
-                           int max_iter, blfmm_solve_stats* stats) {
-  using namespace blfmm_gpu;
+namespace blfmm_gpu {
+namespace {
+// the shared body of blfmm_solve / blfmm_solve_dense: device vectors, the
+// Krylov loop, the best iterate back to the host even when it throws
+int solve_body(long long n, const std::function<Apply(cudaStream_t)>& make_apply, int method,
+               const double* b, double* x, double tol, int max_iter, blfmm_solve_stats* stats) {
   blfmm_solve_stats st{};
   int rc = BLFMM_OK;
   try {
-    if (!plan) throw Error(BLFMM_EINVAL, "null plan");
-    blfmm_plan_info info;
-    ckb(blfmm_plan_get_info(plan, &info));
-    if (info.nrhs != 1) throw Error(BLFMM_EINVAL, "the solver takes a one right-hand-side plan");
-    if (info.n && (!b || !x)) throw Error(BLFMM_EINVAL, "null rhs / solution");
+    if (n && (!b || !x)) throw Error(BLFMM_EINVAL, "null rhs / solution");
     if (!(tol > 0.0)) throw Error(BLFMM_EINVAL, "tol must be positive");
     if (method != BLFMM_SOLVE_CG && method != BLFMM_SOLVE_GMRES)
       throw Error(BLFMM_EINVAL, "unknown Krylov method");
@@ -281,21 +285,22 @@ extern "C" int blfmm_solve(blfmm_plan* plan, int method, const double* b, double
       cudaStream_t s;
       ~StreamGuard() { cudaStreamDestroy(s); }
     } sg{s};
-    Vecs v(info.n, s);
+    const Apply apply = make_apply(s);
+    Vecs v(n, s);
     double* db = v.alloc();
     double* dx = v.alloc();
-    if (info.n) ck(cudaMemcpyAsync(db, b, sizeof(double) * info.n, cudaMemcpyHostToDevice, s));
+    if (n) ck(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     try {
-      if (method == BLFMM_SOLVE_CG) run_cg(plan, v, db, dx, tol, max_iter, st);
-      else run_gmres(plan, v, db, dx, tol, max_iter, st);
+      if (method == BLFMM_SOLVE_CG) run_cg(apply, v, db, dx, tol, max_iter, st);
+      else run_gmres(apply, v, db, dx, tol, max_iter, st);
     } catch (const Error&) {
-      if (info.n) {  // the best iterate so far, as the reference's result
-        cudaMemcpyAsync(x, dx, sizeof(double) * info.n, cudaMemcpyDeviceToHost, s);
+      if (n) {  // the best iterate so far, as the reference's result
+        cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
       }
       throw;
     }
-    if (info.n) ck(cudaMemcpyAsync(x, dx, sizeof(double) * info.n, cudaMemcpyDeviceToHost, s));
+    if (n) ck(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     ck(cudaStreamSynchronize(s));
   } catch (const Error& e) {
     set_error(e);
@@ -308,5 +313,75 @@ extern "C" int blfmm_solve(blfmm_plan* plan, int method, const double* b, double
     rc = BLFMM_EINVAL;
   }
   if (stats) *stats = st;
+  return rc;
+}
+}  // namespace
+}  // namespace blfmm_gpu
+
+extern "C" int blfmm_solve(blfmm_plan* plan, int method, const double* b, double* x, double tol,
+                           int max_iter, blfmm_solve_stats* stats) {
+  using namespace blfmm_gpu;
+  blfmm_plan_info info{};
+  try {
+    if (!plan) throw Error(BLFMM_EINVAL, "null plan");
+    ckb(blfmm_plan_get_info(plan, &info));
+    if (info.nrhs != 1) throw Error(BLFMM_EINVAL, "the solver takes a one right-hand-side plan");
+  } catch (const Error& e) {
+    set_error(e);
+    if (stats) *stats = blfmm_solve_stats{};
+    return e.code;
+  }
+  return solve_body(
+      info.n,
+      [plan](cudaStream_t s) -> Apply {
+        return [plan, s](const double* in, double* out) {
+          ckb(blfmm_execute_device(plan, in, out, nullptr, s));
+        };
+      },
+      method, b, x, tol, max_iter, stats);
+}
+
+// solve_interpolation, Backend::dense (solver.cpp:207-262, 269-275): the same
+// Krylov loops on the dense kernel matrix A_ij = phi(|x_i - x_j|), applied
+// matrix-free on the device (k_direct) instead of assembled; every
+// RadialKernel type; N <= 8192 as assemble_dense (std::length_error beyond).
+extern "C" int blfmm_solve_dense(int d, long long n, const double* coords, int kernel_type,
+                                 double shape, int method, const double* b, double* x,
+                                 double tol, int max_iter, blfmm_solve_stats* stats,
+                                 int device) {
+  using namespace blfmm_gpu;
+  double* dcoords = nullptr;
+  int prev = -1;
+  try {
+    if (d < 1 || d > 3) throw Error(BLFMM_EINVAL, "d must be 1, 2 or 3");
+    if (n < 0) throw Error(BLFMM_EINVAL, "n must be >= 0");
+    if (n > 8192) throw Error(BLFMM_ELENGTH, "dense assembly capped at N=8192");
+    if (n && !coords) throw Error(BLFMM_EINVAL, "null coordinates");
+    require_radial_kernel(KernelSpec{kernel_type, shape});
+    if (device >= 0) {
+      ck(cudaGetDevice(&prev));
+      ck(cudaSetDevice(device));
+    }
+    if (n) {
+      ck(cudaMalloc(&dcoords, sizeof(double) * n * d));
+      ck(cudaMemcpy(dcoords, coords, sizeof(double) * n * d, cudaMemcpyHostToDevice));
+    }
+  } catch (const Error& e) {
+    set_error(e);
+    if (dcoords) cudaFree(dcoords);
+    if (prev >= 0) cudaSetDevice(prev);
+    if (stats) *stats = blfmm_solve_stats{};
+    return e.code;
+  }
+  const int rc = solve_body(
+      n,
+      [=](cudaStream_t s) -> Apply {
+        return [=](const double* in, double* out) {
+          direct_device(d, n, dcoords, kernel_type, shape, in, out, s);
+        };
+      },
+      method, b, x, tol, max_iter, stats);
+  if (dcoords) cudaFree(dcoords);
+  if (prev >= 0) cudaSetDevice(prev);
   return rc;
 }

@@ -311,6 +311,16 @@ void require_fmm_kernel(const KernelSpec& k) {
                 "kernel not supported by the GPU band-limited FMM (gaussian, mq, imq)");
 }
 
+void require_radial_kernel(const KernelSpec& k) {
+  if (k.type < BLFMM_KERNEL_GAUSSIAN || k.type > BLFMM_KERNEL_WENDLAND31)
+    throw Error(BLFMM_EINVAL, "unknown kernel type");
+  if (!(k.shape > 0.0) || !std::isfinite(k.shape))
+    throw Error(BLFMM_EINVAL, "kernel parameter must be positive");
+  if (k.type == BLFMM_KERNEL_TPS &&
+      (k.shape != std::floor(k.shape) || std::fmod(k.shape, 2.0) != 0.0))
+    throw Error(BLFMM_EINVAL, "tps beta must be a positive even integer");
+}
+
 double fourier_value(const KernelSpec& k, double xi, int d) {
   if (d < 1 || d > 3) throw Error(BLFMM_EINVAL, "d must be 1, 2 or 3");
   xi = std::abs(xi);

@@ -218,7 +218,6 @@ def _device_apply(plan: Plan):
 
 def solve_interpolation(prob: InterpolationProblem):
     """solver.cpp:243-300. Returns (lambda [numpy], SolveStats)."""
-    import torch
     if prob.ps is None:
         raise InvalidArgument("problem has no point set")
     ps = prob.ps
@@ -237,15 +236,30 @@ def solve_interpolation(prob: InterpolationProblem):
         level = prob.leaf_level if prob.leaf_level > 0 else default_leaf_level(n, ps.d, multilevel)
         plan = Plan(ps, level, prob.kernel, sigma, m)
         return solve_on_plan(plan, rhs, prob.tol, prob.max_iter, positive_definite(prob.kernel))
-    dev = torch.device("cuda")
+    # Backend.dense (the reference assembles the matrix with Eigen, solver.cpp:
+    # 207-262): the same loops in the library on the matrix-free O(N^2) device
+    # kernel (blfmm_solve_dense), every kernel type, N <= 8192
+    return solve_dense(prob.kernel, ps, rhs, prob.tol, prob.max_iter)
 
-    def apply(x):
-        xv = x.detach().cpu().numpy()
-        return torch.from_numpy(direct_matvec(prob.kernel, ps, xv).values).to(dev)
-    b = torch.from_numpy(rhs).to(dev)
-    runner = run_cg if positive_definite(prob.kernel) else run_gmres
-    x, stats = runner(apply, b, prob.tol, prob.max_iter)
-    return x.cpu().numpy(), stats
+
+def solve_dense(kernel, ps, rhs, tol: float, max_iter: int):
+    """blfmm_solve_dense: CG / restarted GMRES on A_ij = phi(|x_i - x_j|)."""
+    import ctypes as ct
+    rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+    coords = np.ascontiguousarray(ps.pts, dtype=np.float64)
+    x = np.zeros_like(rhs)
+    st = _capi.SolveStatsC()
+    spd = positive_definite(kernel)
+    dp = ct.POINTER(ct.c_double)
+    rc = _capi.lib().blfmm_solve_dense(
+        ps.d, ps.size(), coords.ctypes.data_as(dp), int(kernel.type), float(kernel.shape),
+        _capi.SOLVE_CG if spd else _capi.SOLVE_GMRES, rhs.ctypes.data_as(dp),
+        x.ctypes.data_as(dp), float(tol), int(max_iter), ct.byref(st), -1)
+    stats = SolveStats(iterations=st.iterations, residual=st.residual, matvecs=st.matvecs,
+                       method="cg" if st.method == _capi.SOLVE_CG else "gmres",
+                       converged=bool(st.converged))
+    _capi.check(rc)
+    return x, stats
 
 
 def solve_on_plan(plan: Plan, rhs, tol: float, max_iter: int, spd: bool):

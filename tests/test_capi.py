@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_capi.EXPORTS), "ctypes table out of sync with the header"
-    assert _capi.lib().blfmm_abi_version() == 3
+    assert _capi.lib().blfmm_abi_version() == 4
 
 
 def test_library_is_sm100a():

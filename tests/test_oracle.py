@@ -311,6 +311,32 @@ def test_direct_matches_reference(oracle):
         assert rel_l2(v, rv) <= 1e-15 and near == 700 * 700
 
 
+def test_eval_kernel_tps_wendland_reference_values(oracle):
+    """eval_kernel for the kernel types outside the FMM plan (TPS, Wendland;
+    kernels.cpp:141-158), used by the O(N^2) sum and the dense Krylov backend:
+    the reference's own checks (test_kernels.cpp:79-98)."""
+    ek = oracle.eval_kernel
+    assert ek("tps:beta=2", 0.0) == 0.0
+    assert ek("tps:beta=2", 0.5) == pytest.approx(0.25 * math.log(0.5), rel=1e-15)
+    assert ek("tps:beta=4", 2.0) == pytest.approx(-16.0 * math.log(2.0), rel=1e-15)
+    assert ek("wendland:eps=1", 0.0) == pytest.approx(1.0)
+    assert ek("wendland:eps=1", 0.5) == pytest.approx(0.5 ** 4 * 3.0, rel=1e-15)
+    assert ek("wendland:eps=1", 1.0) == 0.0 and ek("wendland:eps=1", 2.0) == 0.0
+    assert ek("wendland31:eps=0.5", 1.0) == pytest.approx(0.5 ** 3 * 2.5, rel=1e-15)
+    assert ek("wendland31:eps=0.5", 2.0) == 0.0
+    assert ek("tps", 0.5) == ek("tps:beta=2", 0.5)  # parse_kernel_spec default beta = 2
+
+
+@needs_ref
+def test_direct_tps_wendland_matches_reference(oracle):
+    x = I.uniform_points(500, 2, 19)
+    w = I.uniform_weights(500, 20)
+    for spec in ("tps:beta=2", "tps:beta=4", "wendland:eps=2", "wendland31:eps=0.5"):
+        v = oracle.direct(x, w, spec)
+        rv, near = oracle.ref_direct(x, w, spec)
+        assert rel_l2(v, rv) <= 1e-15 and near == 500 * 500, spec
+
+
 def test_golden_fixtures_match_oracle(oracle):
     """tests/golden/*.npz were produced by the reference itself
     (tests/golden/make_golden.py); the oracle must reproduce them."""

@@ -71,6 +71,75 @@ def test_gmres_on_mq_and_validation(blfmm):
         S.solve_interpolation(S.InterpolationProblem(k, ps, rhs, tol=0.0))
 
 
+@pytest.mark.gpu
+def test_direct_every_kernel_type_matches_oracle(blfmm, oracle):
+    """blfmm_direct evaluates every RadialKernel type (eval_kernel,
+    kernels.cpp:131-161): TPS and the Wendland functions against the CPU
+    restatement (pinned on the reference's own values), d = 1, 2, 3."""
+    for d in (1, 2, 3):
+        x = I.uniform_points(900, d, 40 + d)
+        x[7] = x[3]  # a coincident pair: phi(0) (TPS: 0)
+        w = I.uniform_weights(900, 50 + d)
+        ps = blfmm.PointSet(d, x)
+        for spec in ("tps:beta=2", "tps:beta=4", "wendland:eps=1.5", "wendland31:eps=0.5"):
+            v = blfmm.direct_matvec(blfmm.parse_kernel_spec(spec), ps, w).values
+            ov = oracle.direct(x, w, spec)
+            assert np.linalg.norm(v - ov) <= 1e-14 * np.linalg.norm(ov), (d, spec)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec,d,n,method", [("gaussian:c=400", 2, 300, "cg"),
+                                             ("imq:c=0.01", 1, 200, "cg"),
+                                             ("wendland:eps=4", 2, 400, "cg"),
+                                             ("wendland31:eps=20", 1, 150, "cg"),
+                                             ("tps:beta=2", 1, 200, "gmres"),
+                                             ("mq:c=0.02", 3, 250, "gmres")])
+def test_dense_backend_in_the_library(blfmm, oracle, spec, d, n, method):
+    """Backend::dense (solver.cpp:207-262, the reference's default): the Krylov
+    loop runs in the library on the matrix-free O(N^2) device kernel
+    (blfmm_solve_dense) for every kernel type. The solution satisfies the
+    dense system assembled on the CPU with the oracle's eval_kernel; CG for the
+    positive definite kernels (kernels.cpp:334-337), GMRES otherwise. (Shape
+    parameters keep cond(A) between 1e3 and 2e6.)"""
+    if d == 1:
+        x = I.generate_quasiuniform(n, 1, 700 + n, 0.3)
+    else:
+        x = I.uniform_points(n, d, 600 + n)
+    ps = blfmm.PointSet(d, x)
+    k = blfmm.parse_kernel_spec(spec)
+    rhs = np.sin(math.pi * x[:, 0]) + 0.25 * np.cos(2.0 * x.sum(axis=1))
+    tol = 1e-9
+    lam, st = S.solve_interpolation(S.InterpolationProblem(k, ps, rhs, S.Backend.dense, tol=tol,
+                                                           max_iter=4000))
+    assert st.method == method and st.converged and st.residual <= tol
+    r = np.linalg.norm(x[:, None, :] - x[None, :, :], axis=2)
+    A = np.vectorize(lambda v: oracle.eval_kernel(spec, v))(r)
+    assert np.linalg.norm(A @ lam - rhs) <= 20 * tol * np.linalg.norm(rhs)
+
+
+@pytest.mark.gpu
+def test_dense_backend_limits_and_errors(blfmm):
+    """assemble_dense's N <= 8192 cap (std::length_error), accuracy_error with
+    the best residual when max_iter is too small (test_solver.cpp:170-195),
+    argument validation."""
+    k = blfmm.parse_kernel_spec("tps:beta=2")
+    x = I.generate_quasiuniform(64, 1, 901, 0.3)
+    ps = blfmm.PointSet(1, x)
+    rhs = np.sin(math.pi * x[:, 0])
+    with pytest.raises(blfmm.AccuracyError) as e:
+        S.solve_interpolation(S.InterpolationProblem(k, ps, rhs, S.Backend.dense, tol=1e-12,
+                                                     max_iter=2))
+    assert 0.0 < e.value.achieved < 10.0
+    big = blfmm.PointSet(1, I.uniform_points(8193, 1, 3))
+    with pytest.raises(blfmm.LengthError):
+        S.solve_interpolation(S.InterpolationProblem(k, big, np.zeros(8193), S.Backend.dense))
+    with pytest.raises(blfmm.InvalidArgument):
+        S.solve_dense(blfmm.RadialKernel(blfmm.KernelType.TPS, 3.0), ps, rhs, 1e-8, 10)
+    # the FMM plan still takes the north star's three kernels only
+    with pytest.raises(blfmm.DomainError):
+        blfmm.Plan(ps, 3, k, math.pi, 16)
+
+
 def test_default_leaf_level_rules():
     """d <= 2 keeps the reference's rules (blfmm_cli.cpp:377-380, solver.cpp);
     d = 3 counts 8^L boxes and stays inside the d*L <= 24 cap."""
