@@ -131,6 +131,27 @@ def test_solve_writes_converged_coefficients(tmp_path, fixture_files):
 
 
 @pytest.mark.gpu
+def test_solve_reference_case_tps_dense(tmp_path, fixture_files):
+    """test_cli.cpp:293-318 verbatim: `solve --kernel tps:beta=2 --backend dense
+    --tol 1e-8` converges with GMRES; `--max-iter 2` fails with a one-line JSON
+    error carrying "achieved" and exit code 1."""
+    pts, _, rhs = fixture_files
+    lam = tmp_path / "lambda.csv"
+    rc, _, err = run_cli(["solve", "--kernel", "tps:beta=2", "--points", str(pts), "--rhs",
+                          str(rhs), "--backend", "dense", "--tol", "1e-8", "--out", str(lam)],
+                         tmp_path)
+    assert rc == 0, err
+    text = open(lam).read()
+    assert read_values(lam).size == 256
+    assert "# method: gmres" in text and "# converged: 1" in text
+    rc, _, err = run_cli(["solve", "--kernel", "tps:beta=2", "--points", str(pts), "--rhs",
+                          str(rhs), "--backend", "dense", "--tol", "1e-8", "--max-iter", "2",
+                          "--out", str(lam)], tmp_path)
+    assert rc == 1
+    assert '"achieved"' in err and err.find("\n") == len(err) - 1  # single line
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("dim", [1, 2])
 def test_fmm_matvec_outputs_match_reference(tmp_path, oracle, dim):
     """The CLI's artifacts against the REFERENCE library (compiled from its
