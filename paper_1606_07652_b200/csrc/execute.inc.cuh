@@ -150,11 +150,9 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
   const long long np2m = phase == 1 ? p->n_eleaf : leaf.nbox;
   if (up && np2m) {
     if (D == 1) {
-      int batch = static_cast<int>(std::min<long long>(
-          32, std::max<long long>(1, (40 * 1024) / (D * M * (long long)sizeof(double2) + 8))));
-      size_t smem = (size_t)batch * D * M * sizeof(double2) + batch * sizeof(double);
-      if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(k_p2m<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      // (d = 1 forms the phases in registers: no staged rows, any M)
+      const int batch = 1;
+      const size_t smem = 0;
       dim3 grid((unsigned)np2m, blocks_for(K, kP2MThreads * kP2MNodesPerThread), R);
       k_p2m<D><<<grid, kP2MThreads, smem, st>>>(
           leaf_list, leaf.key.as<uint32_t>(), p->leaf_start.as<int>(), x0, x1, x2, p->lam.as<double>(),
@@ -517,11 +515,9 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
   // L2P
   if (leaf.nbox) {
     if (D == 1) {
-      // 8 points per batch unless their phase tables would not fit in shared memory
-      auto launch1 = [&](auto kern, int batch) {
-        size_t smem = (size_t)batch * D * M * sizeof(double2);
-        if (smem > 48 * 1024)
-          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      // 8 points per batch
+      auto launch1 = [&](auto kern, int) {
+        const size_t smem = 0;  // d = 1: phases in registers
         dim3 grid((unsigned)leaf.nbox, R);
         kern<<<grid, kL2PThreads, smem, st>>>(
             leaf.key.as<uint32_t>(), p->leaf_start.as<int>(), x0, x1, x2, leaf.loc.as<double2>(),
@@ -529,8 +525,7 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
             side[1], side[2], p->weight, p->far_.as<double>(),
             p->imag_bits.as<unsigned long long>());
       };
-      if ((size_t)8 * M * sizeof(double2) <= 200 * 1024) launch1(k_l2p<D, 8>, 8);
-      else launch1(k_l2p<D, 1>, 1);
+      launch1(k_l2p<D, 8>, 8);
     } else if (D == 3 && p->mr) {
       auto l2pm = p->want_imag ? k_l2p_mr<true> : k_l2p_mr<false>;
       const int smem = (int)(sizeof(double2) * (kMRSpan * kMRRow + 2 * 32 * kMRLS));

@@ -33,15 +33,29 @@ __global__ void __launch_bounds__(kL2PThreads)
   for (int pb = p0; pb < p1; pb += kL2PBatch) {
     int nb = min(kL2PBatch, p1 - pb);
     __syncthreads();
+    double2 part[kL2PBatch];
+#pragma unroll
+    for (int j = 0; j < kL2PBatch; ++j) part[j] = make_double2(0.0, 0.0);
+    if (D == 1) {
+      // d = 1: node = m and each point-node phase is used once: formed in
+      // registers (no staged rows, any M); same operations as the staged form
+      double rk[kL2PBatch];
+#pragma unroll
+      for (int j = 0; j < kL2PBatch; ++j) rk[j] = j < nb ? x0[pb + j] - xa[0] : 0.0;
+      for (long long e = threadIdx.x; e < K; e += blockDim.x) {
+        const double2 lv = la[e];
+        const double xe = xi[e];
+#pragma unroll
+        for (int j = 0; j < kL2PBatch; ++j)
+          if (j < nb) cmac(part[j], polar1(xe * rk[j]), lv);
+      }
+    } else {
     for (int t = threadIdx.x; t < nb * D * M; t += blockDim.x) {
       int j = t / (D * M), k = (t / M) % D, m = t % M;
       double rk = xs[k][pb + j] - xa[k];
       ph[t] = polar1(xi[m] * rk);
     }
     __syncthreads();
-    double2 part[kL2PBatch];
-#pragma unroll
-    for (int j = 0; j < kL2PBatch; ++j) part[j] = make_double2(0.0, 0.0);
     for (long long e = threadIdx.x; e < K; e += blockDim.x) {
       int mk[3];
       long long t = e;
@@ -60,6 +74,7 @@ __global__ void __launch_bounds__(kL2PThreads)
           cmac(part[j], p, lv);
         }
       }
+    }
     }
 #pragma unroll
     for (int j = 0; j < kL2PBatch; ++j) {

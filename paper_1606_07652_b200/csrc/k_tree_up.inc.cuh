@@ -206,6 +206,24 @@ __global__ void __launch_bounds__(kP2MThreads)
       t /= M;
     }
   }
+  if (D == 1) {
+    // d = 1: node = m, every point-node phase is used by exactly one thread, so
+    // it is formed in registers (no staged rows: any M fits, e.g. the 16,384
+    // nodes of test_solver.cpp:244-285); same operations as the staged form
+    double xq[kP2MNodesPerThread];
+#pragma unroll
+    for (int q = 0; q < kP2MNodesPerThread; ++q) xq[q] = xi[mk[q][0]];
+    for (int j = p0; j < p1; ++j) {
+      const double rk = xb[0] - x0[j];
+      const double w = lam[(long long)r * n + j];
+#pragma unroll
+      for (int q = 0; q < kP2MNodesPerThread; ++q) {
+        const double2 p = polar1(xq[q] * rk);
+        acc[q].x = fma(w, p.x, acc[q].x);
+        acc[q].y = fma(w, p.y, acc[q].y);
+      }
+    }
+  } else
   for (int pb = p0; pb < p1; pb += batch) {
     int nb = min(batch, p1 - pb);
     __syncthreads();

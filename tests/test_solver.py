@@ -140,6 +140,88 @@ def test_dense_backend_limits_and_errors(blfmm):
         blfmm.Plan(ps, 3, k, math.pi, 16)
 
 
+def _jittered48(blfmm):
+    """test_solver.cpp:14-20: jittered(48, 0, 48, seed 44, jitter 0.4)."""
+    x = I.generate_quasiuniform(48, 1, 44, 0.4, lo=(0.0, 0.0), hi=(48.0, 1.0))
+    return x, blfmm.PointSet(1, x, blfmm.BoundingBox((0.0, 0.0, 0.0), (48.0, 1.0, 1.0)))
+
+
+@pytest.mark.gpu
+def test_reference_solve_cases_default_backend(blfmm):
+    """The reference's solve_interpolation tests on its default (dense) backend,
+    test_solver.cpp:132-170 and 172-194: unit-vector weights recovered from
+    their own rhs; the reported residual reproducible from a direct recompute;
+    exhausting max_iter raises with the best residual (CG and GMRES)."""
+    k = blfmm.parse_kernel_spec("imq:c=1")
+    x, ps = _jittered48(blfmm)
+    ek = np.zeros(48)
+    ek[17] = 1.0
+    b = blfmm.direct_matvec(k, ps, ek).values
+    lam, st = S.solve_interpolation(S.InterpolationProblem(k, ps, b, S.Backend.dense, tol=1e-12))
+    assert st.method == "cg" and st.converged and st.matvecs >= st.iterations
+    assert np.abs(lam - ek).max() < 1e-8
+    rhs = np.sin(math.pi * x[:, 0] / 48.0)
+    lam, st = S.solve_interpolation(S.InterpolationProblem(k, ps, rhs, S.Backend.dense, tol=1e-12))
+    u = blfmm.direct_matvec(k, ps, lam).values
+    recomputed = np.linalg.norm(u - rhs) / np.linalg.norm(rhs)
+    assert st.residual <= 1e-12 and abs(st.residual - recomputed) < 1e-12
+    with pytest.raises(blfmm.AccuracyError) as e:
+        S.solve_interpolation(S.InterpolationProblem(k, ps, np.ones(48), S.Backend.dense,
+                                                     tol=1e-12, max_iter=3))
+    assert 0.0 < e.value.achieved < 10.0 and "tolerance" in str(e.value)
+    with pytest.raises(blfmm.AccuracyError):
+        S.solve_interpolation(S.InterpolationProblem(blfmm.parse_kernel_spec("tps:beta=2"), ps,
+                                                     np.ones(48), S.Backend.dense, tol=1e-12,
+                                                     max_iter=2))
+
+
+@pytest.mark.gpu
+def test_reference_fmm_backend_perturbation_bound(blfmm, oracle):
+    """test_solver.cpp:244-285: the single-level FMM backend's solution differs
+    from the dense one by at most the FMM operator's defect amplified by
+    1 / gamma_min (sigma = 12, 16,384 nodes, 48 points on [0, 48])."""
+    k = blfmm.parse_kernel_spec("imq:c=1")
+    x, ps = _jittered48(blfmm)
+    rhs = np.sin(math.pi * x[:, 0] / 48.0)
+    out = {}
+    for be in (S.Backend.dense, S.Backend.single_fmm):
+        lam, st = S.solve_interpolation(S.InterpolationProblem(k, ps, rhs, be, tol=1e-12,
+                                                               sigma=12.0, m_per_dim=16384))
+        assert st.method == "cg"
+        out[be] = lam
+    ld, lf = out[S.Backend.dense], out[S.Backend.single_fmm]
+    r = np.abs(x[:, 0][:, None] - x[:, 0][None, :])
+    A = 1.0 / np.sqrt(r * r + 1.0)
+    gamma_min = np.linalg.eigvalsh(A).min()
+    assert gamma_min > 0.05
+    defect = blfmm.direct_matvec(k, ps, lf).values - rhs
+    bound = (np.linalg.norm(defect) + 1e-12 * np.linalg.norm(rhs)) / gamma_min * (1.0 + 1e-9)
+    assert np.linalg.norm(ld - lf) <= bound
+    assert np.abs(ld - lf).max() < 1e-4  # reference: measured 1.96e-5
+
+
+@pytest.mark.gpu
+def test_reference_tps_error_decays_under_node_doubling(blfmm, oracle):
+    """test_solver.cpp:287-314: TPS (GMRES, dense backend) interpolation of
+    sin(pi x) on 25 / 50 / 100 / 200 quasi-uniform nodes; the RMS error on 513
+    lattice points decreases and ends below 1e-4 (reference: 2.9e-5)."""
+    k = blfmm.parse_kernel_spec("tps:beta=2")
+    prev = 1e9
+    xe = np.arange(513) / 512.0
+    for n in (25, 50, 100, 200):
+        x = I.generate_quasiuniform(n, 1, 900 + n, 0.3)
+        ps = blfmm.PointSet(1, x)
+        lam, st = S.solve_interpolation(S.InterpolationProblem(
+            k, ps, np.sin(math.pi * x[:, 0]), S.Backend.dense, tol=1e-8))
+        assert st.method == "gmres" and st.converged
+        r = np.abs(xe[:, None] - x[:, 0][None, :])
+        phi = np.where(r > 0, r * r * np.log(np.where(r > 0, r, 1.0)), 0.0)
+        rms = math.sqrt(np.mean((phi @ lam - np.sin(math.pi * xe)) ** 2))
+        assert rms < prev
+        prev = rms
+    assert prev < 1e-4
+
+
 def test_default_leaf_level_rules():
     """d <= 2 keeps the reference's rules (blfmm_cli.cpp:377-380, solver.cpp);
     d = 3 counts 8^L boxes and stays inside the d*L <= 24 cap."""
