@@ -308,6 +308,42 @@ def test_sharded_plans_assemble_to_full(blfmm, name, n, leaf):
         assert sum(owned) == n
 
 
+def test_reference_acceptance_criteria_matvec(blfmm):
+    """The reference's acceptance gate on the matvec path (acceptance.cpp:92-224,
+    criteria 3 and 4) on the GPU backend. Fixture: imq:c=1, 256 quasi-uniform
+    1-D points (seed 11, jitter 0.35), weights 2 u - 1 (seed 12), leaf level 3.
+    3: the single-level matvec against the hybrid direct oracle (original
+    kernel in the neighbour block, Phi_sigma outside): rel Linf < 1e-3 at
+    M = 64 and at least 2x better at M = 128. 4: the multilevel sweep against
+    the single-level sum on shared grids, stencil 10 and the global stencil
+    K = M = 64: rel Linf <= 1e-10."""
+    B = blfmm
+    k = B.parse_kernel_spec("imq:c=1")
+    x = I.generate_quasiuniform(256, 1, 11, 0.35)
+    ps = B.PointSet(1, x)
+    w = I.uniform_weights(256, 12)
+    tree = B.build_tree(ps, 3)
+    hybrid = B.direct_matvec_hybrid(k, ps, tree, w, math.pi).values
+    scale = np.abs(hybrid).max()
+    s64 = B.fmm_matvec_single(B.SumRequest(k, math.pi, ps, w, 64), tree).values
+    s128 = B.fmm_matvec_single(B.SumRequest(k, math.pi, ps, w, 128), tree).values
+    r64 = np.abs(s64 - hybrid).max() / scale
+    r128 = np.abs(s128 - hybrid).max() / scale
+    assert r64 < 1e-3 and r64 / r128 >= 2.0, (r64, r128)
+    for stencil in (10, 64):
+        g = B.make_level_grids(k, math.pi, 64, 1, 3, B.GridMode.shared, stencil)
+        m = B.mlfmm_matvec(B.SumRequest(k, math.pi, ps, w, 64), tree, g).values
+        assert np.abs(m - s64).max() / scale <= 1e-10, stencil
+    # context line of criterion 4: scaled grids are a coarser far-field model,
+    # the same gap under either stencil
+    gaps = []
+    for stencil in (10, 64):
+        g = B.make_level_grids(k, math.pi, 64, 1, 3, B.GridMode.scaled, stencil)
+        m = B.mlfmm_matvec(B.SumRequest(k, math.pi, ps, w, 64), tree, g).values
+        gaps.append(np.abs(m - s64).max() / scale)
+    assert abs(gaps[0] - gaps[1]) <= 0.2 * max(gaps)
+
+
 def test_cpp_adapter_dropin_against_reference():
     """include/blfmm_gpu.hpp + the reference library (built from its own
     sources) in one C++ program: the GPU matvec on the reference's own
