@@ -344,6 +344,34 @@ def test_reference_acceptance_criteria_matvec(blfmm):
     assert abs(gaps[0] - gaps[1]) <= 0.2 * max(gaps)
 
 
+def test_reference_acceptance_structural_properties(blfmm):
+    """acceptance.cpp:351-394 on the GPU backend: M2M conserves the
+    zero-frequency coefficient in both grid modes (node 4 of the M = 8 grid is
+    xi = 0 exactly; parent = sum of its children to 1e-14), and the single-level
+    matvec is linear in the weights to 1e-12 of its scale."""
+    B = blfmm
+    k = B.parse_kernel_spec("gaussian:c=1")
+    x = I.generate_quasiuniform(48, 1, 19, 0.5)
+    ps = B.PointSet(1, x)
+    w = I.uniform_weights(48, 20)
+    tree = B.build_tree(ps, 3)
+    for mode in (B.GridMode.shared, B.GridMode.scaled):
+        grids = B.make_level_grids(k, math.pi, 8, 1, 3, mode, 4)
+        assert grids.grids[2].nodes[4][0] == 0.0
+        exps = B.upsweep(tree, grids, ps, w)
+        for b in range(4):
+            kids = exps[3][2 * b, 4] + exps[3][2 * b + 1, 4]  # children(2, b) = {2b, 2b + 1}
+            assert abs(exps[2][b, 4] - kids) <= 1e-14, (mode, b)
+    k = B.parse_kernel_spec("imq:c=1")
+    x = I.generate_quasiuniform(128, 1, 21, 0.4)
+    ps = B.PointSet(1, x)
+    tree = B.build_tree(ps, 2)
+    wa, wb = I.uniform_weights(128, 22), I.uniform_weights(128, 23)
+    u = [B.fmm_matvec_single(B.SumRequest(k, math.pi, ps, v, 32), tree).values
+         for v in (wa, wb, 2.0 * wa - 3.0 * wb)]
+    assert np.abs(2.0 * u[0] - 3.0 * u[1] - u[2]).max() <= 1e-12 * np.abs(u[2]).max()
+
+
 def test_cpp_adapter_dropin_against_reference():
     """include/blfmm_gpu.hpp + the reference library (built from its own
     sources) in one C++ program: the GPU matvec on the reference's own
