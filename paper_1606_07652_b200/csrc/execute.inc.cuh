@@ -511,6 +511,11 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
     CK(cudaGetLastError());
     p->times.launches[3]++;
   }
+  if (down && p->n_zero_far) {
+    k_zero_boxes<<<dim3((unsigned)p->n_zero_far, R), 256, 0, st>>>(
+        leaf.loc.as<double2>(), p->zero_far.as<int>(), K, leaf.nbox);
+    CK(cudaGetLastError());
+  }
   mark(4);
   // L2P
   if (leaf.nbox) {

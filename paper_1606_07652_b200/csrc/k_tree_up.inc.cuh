@@ -164,6 +164,14 @@ __global__ void k_scatter_sorted(const double* __restrict__ us, const int* __res
   for (int r = 0; r < R; ++r) out[r * n + i] = us[r * n + s];
 }
 
+// locals of the leaves whose interaction lists are empty at every level
+// (plan_build: zero_far): the reference's exact zero
+__global__ void k_zero_boxes(double2* __restrict__ loc, const int* __restrict__ slots, long long K,
+                             long long nbox) {
+  double2* o = loc + ((long long)blockIdx.y * nbox + slots[blockIdx.x]) * K;
+  for (long long t = threadIdx.x; t < K; t += blockDim.x) o[t] = make_double2(0.0, 0.0);
+}
+
 // ---------------------------------------------------------------- P2M
 // V_b[m] = sum_{j in b} lambda_j e^{i xi_m . (x_b - x_j)}  (mlfmm.cpp:218-231)
 // One CTA per (leaf, node tile, rhs); per-axis phase tables of a batch of

@@ -450,6 +450,20 @@ void plan_build_tree(blfmm_plan* p, const double* coords_host) {
     }
     for (long long a = 0; a < leaf.nbox; ++a)
       p->max_leaf_pts = std::max(p->max_leaf_pts, hstart[a + 1] - hstart[a]);
+    // Leaves whose 3^d neighbourhood holds EVERY point: their interaction lists
+    // are empty at every level and the reference's far field there is an exact
+    // zero. The neighbourhood-difference sweep would leave
+    // eps |C| |NS| instead, which the pole cell of a singular spectrum (MQ:
+    // |C| ~ 1e8 / dxi, the 1e-8 pole ball) lifts above the parity bar when
+    // nothing else contributes; their locals are zeroed before L2P.
+    {
+      std::vector<int> zf;
+      if (leaf.nbox <= (D == 1 ? 3 : (D == 2 ? 9 : 27)))
+        for (long long a = 0; a < leaf.nbox; ++a)
+          if (hsrc[a] == n) zf.push_back(static_cast<int>(a));
+      p->n_zero_far = static_cast<long long>(zf.size());
+      if (!zf.empty()) upload(p->zero_far, zf);
+    }
     // batched right-hand sides: (leaf, first target) per chunk of 32 targets,
     // heaviest (most sources) first
     if (p->R > 1) {

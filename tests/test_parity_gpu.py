@@ -372,6 +372,65 @@ def test_reference_acceptance_structural_properties(blfmm):
     assert np.abs(2.0 * u[0] - 3.0 * u[1] - u[2]).max() <= 1e-12 * np.abs(u[2]).max()
 
 
+def _load_fuzz():
+    import importlib.util
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                        "fuzz_small.py")
+    spec = importlib.util.spec_from_file_location("fuzz_small", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_small_configuration_sweep(blfmm, oracle):
+    """tools/fuzz_small.py as a test: 60 seeded small configurations across the
+    kernel-selection boundaries (d = 1, 2, 3; M from 2 to 20,000 in 1-D, odd /
+    even / 16 / large in 2-D and 3-D; leaf levels 2..4; 1 to 3,000 points
+    uniform, clustered in one neighbourhood, or on the domain faces; 1, 2 or 8
+    right-hand sides) against the oracle: rel-l2 <= 1e-10, near_pairs and
+    far_work exact. (This sweep found the d = 1 staging limit at large M and
+    the clustered-MQ far-field zero below.)"""
+    fz = _load_fuzz()
+    bad = []
+    for d, m, leaf, n, spec, nrhs, dist, s in fz.cases(60, 1):
+        x = fz.points(d, n, dist, s)
+        w = np.random.default_rng(s + 1).uniform(-1, 1, (nrhs, n) if nrhs > 1 else n)
+        res, plan = gpu_mlfmm(blfmm, x, w, spec, math.pi, m, leaf)
+        ctab = blfmm.translation_coefficients(blfmm.parse_kernel_spec(spec),
+                                              blfmm.make_quadrature(math.pi, m, d)).c_vals
+        ov, ost, _ = oracle.mlfmm(x, w, spec, math.pi, m, leaf, c_table_in=ctab)
+        v, ov = np.asarray(res.values).reshape(nrhs, n), np.asarray(ov).reshape(nrhs, n)
+        err = max(rel_l2(v[r], ov[r]) if np.linalg.norm(ov[r]) > 0 else float(np.abs(v[r]).max())
+                  for r in range(nrhs))
+        if not (err <= TOL and res.stats.near_pairs == ost["near_pairs"]
+                and res.stats.far_work == ost["far_work"]):
+            bad.append((d, m, leaf, n, spec, nrhs, dist, err))
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("d,m,leaf,n,nrhs", [(1, 64, 3, 3000, 2), (1, 8, 3, 7, 1), (1, 2, 3, 1, 1),
+                                             (2, 16, 4, 500, 1), (3, 16, 3, 400, 1)])
+def test_clustered_mass_far_field_is_exactly_zero(blfmm, oracle, d, m, leaf, n, nrhs):
+    """All points inside one leaf neighbourhood: every interaction list is empty
+    and the reference's far field is an exact zero. The neighbourhood-difference
+    sweep would leave eps |C| |NS| there, which the MQ pole cell (|C| ~ 1e8 / dxi;
+    2.7e16 in 1-D when xi_{M/2} rounds off zero) lifts far above the parity bar;
+    the plan flags such leaves and their locals are zeroed (k_zero_boxes)."""
+    rng = np.random.default_rng(5 + n)
+    x = np.clip(0.5 + 0.02 * rng.standard_normal((n, d)) / (2 ** (leaf - 3)), 0.0, 1.0)
+    w = rng.uniform(-1, 1, (nrhs, n) if nrhs > 1 else n)
+    spec = "mq:c=0.2"
+    res, plan = gpu_mlfmm(blfmm, x, w, spec, math.pi, m, leaf)
+    ctab = blfmm.translation_coefficients(blfmm.parse_kernel_spec(spec),
+                                          blfmm.make_quadrature(math.pi, m, d)).c_vals
+    ov, ost, _ = oracle.mlfmm(x, w, spec, math.pi, m, leaf, c_table_in=ctab)
+    assert ost["far_work"] == res.stats.far_work
+    v, ov = np.asarray(res.values).reshape(nrhs, n), np.asarray(ov).reshape(nrhs, n)
+    for r in range(nrhs):
+        assert rel_l2(v[r], ov[r]) <= 1e-13, (r, rel_l2(v[r], ov[r]))
+    assert res.stats.max_imag_residual == 0.0 == ost["max_imag_residual"]
+
+
 def test_cpp_adapter_dropin_against_reference():
     """include/blfmm_gpu.hpp + the reference library (built from its own
     sources) in one C++ program: the GPU matvec on the reference's own
