@@ -408,6 +408,20 @@ def test_small_configuration_sweep(blfmm, oracle):
     assert not bad, bad
 
 
+def test_small_mode_sweep(blfmm, oracle):
+    """The second sweep of tools/fuzz_small.py: scaled grids, the single-level
+    sum, a non-unit domain with points outside it, 3 / 5 / 16 / 32 right-hand
+    sides, the stats-free device call (graph replay) - 40 seeded cases against
+    the oracle."""
+    fz = _load_fuzz()
+    bad = []
+    for case in fz.mode_cases(40, 1001):
+        ok, err = fz.run_mode_case(*case)
+        if not ok:
+            bad.append(case + (err,))
+    assert not bad, bad
+
+
 @pytest.mark.parametrize("d,m,leaf,n,nrhs", [(1, 64, 3, 3000, 2), (1, 8, 3, 7, 1), (1, 2, 3, 1, 1),
                                              (2, 16, 4, 500, 1), (3, 16, 3, 400, 1)])
 def test_clustered_mass_far_field_is_exactly_zero(blfmm, oracle, d, m, leaf, n, nrhs):
