@@ -99,7 +99,13 @@ def test_nccl_one_rank_group(blfmm, name, n, leaf, nrhs):
 
 @pytest.mark.parametrize("args", [["3", "60000", "4", "2", "imq:c=0.1", "3.141592653589793", "16", "1"],
                                   ["3", "40000", "4", "3", "gaussian:c=64", "3.141592653589793", "16", "2"],
-                                  ["2", "50000", "5", "4", "mq:c=0.05", "3.141592653589793", "16", "1"]])
+                                  ["2", "50000", "5", "4", "mq:c=0.05", "3.141592653589793", "16", "1"],
+                                  # tools/fuzz_dist.sh: other even M (3-multiplication block-A
+                                  # kernels in exchange mode), odd M, 32 right-hand sides, d = 1
+                                  ["3", "20000", "3", "3", "gaussian:c=64", "3.141592653589793", "34", "1"],
+                                  ["3", "20000", "3", "4", "imq:c=0.1", "3.141592653589793", "15", "1"],
+                                  ["3", "30000", "3", "2", "gaussian:c=64", "3.141592653589793", "16", "32"],
+                                  ["1", "5000", "4", "2", "gaussian:c=9", "3.141592653589793", "300", "2"]])
 def test_cpp_caller_shards_through_the_c_abi(tmp_path, args):
     """A C++ program (tests/cpp/dist_threads.cpp) runs `world` ranks as
     threads, each with its own plan, and supplies host collectives through
