@@ -546,7 +546,8 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
           p->work8.as<int2>(), p->leaf_start.as<int>(), p->pht.as<double2>(),
           leaf.loc.as<double2>(), M, K, n, leaf.nbox, p->weight, p->far_.as<double>(),
           p->himag.as<double>());
-      // block A: 32 points per CTA (16 with the imaginary-residual GEMM)
+      // block A: 8-point tiles with the imaginary-residual GEMM (stats requested), else the
+      // 3-multiplication kernel on class-sorted spans
       auto la = [&](auto kern, const DevBuf& wk, long long nw) {
         kern<<<dim3((unsigned)nw, 1, R), 128, 0, st>>>(
             wk.as<int2>(), p->leaf_start.as<int>(), p->pht.as<double2>(), leaf.loc.as<double2>(),

@@ -591,11 +591,6 @@ void plan_build_tree(blfmm_plan* p, const double* coords_host) {
       for (int t = hstart[a]; t < hstart[a + 1]; t += kL2PSpan) w128.push_back(make_int2((int)a, t));
     upload(p->work128, w128);
     p->nwork128 = static_cast<long long>(w128.size());
-    std::vector<int2> w32;
-    for (long long a : order)
-      for (int t = hstart[a]; t < hstart[a + 1]; t += 32) w32.push_back(make_int2((int)a, t));
-    upload(p->work32, w32);
-    p->nwork32 = static_cast<long long>(w32.size());
     std::vector<int2> w64;
     for (long long a : order)
       for (int t = hstart[a]; t < hstart[a + 1]; t += kMRSpan) w64.push_back(make_int2((int)a, t));
