@@ -207,10 +207,15 @@ void launch_all(blfmm_plan* p, const double* d_lam_in, double* d_out, int phase 
             leaf.nbox, leaf.mult.as<double2>(), H, H, kGroups);
       }
       const int smx = (int)(sizeof(double2) * kBigPts * 64);
-      CK(cudaFuncSetAttribute(k_p2m_axes, cudaFuncAttributeMaxDynamicSharedMemorySize, smx));
-      k_p2m_axes<<<dim3((unsigned)np2m, 3, R), 256, smx, st>>>(
+      // block C: M <= 64 columns (8 tiles); blocks B1 / B2: H - 1 <= 31 columns (4 tiles)
+      CK(cudaFuncSetAttribute(k_p2m_axes<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smx));
+      CK(cudaFuncSetAttribute(k_p2m_axes<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smx));
+      k_p2m_axes<8><<<dim3((unsigned)np2m, 1, R), 256, smx, st>>>(
           leaf_list, p->leaf_start.as<int>(), p->pht.as<double2>(), p->lam.as<double>(), M, K, n,
-          leaf.nbox, leaf.mult.as<double2>());
+          leaf.nbox, leaf.mult.as<double2>(), 0);
+      k_p2m_axes<4><<<dim3((unsigned)np2m, 2, R), 256, smx, st>>>(
+          leaf_list, p->leaf_start.as<int>(), p->pht.as<double2>(), p->lam.as<double>(), M, K, n,
+          leaf.nbox, leaf.mult.as<double2>(), 1);
       if (p->hK < K)  // padding nodes stay zero
         CK(cudaMemset2DAsync(leaf.mult.as<double2>() + p->hK, sizeof(double2) * K, 0,
                              sizeof(double2) * (K - p->hK), (size_t)R * leaf.nbox, st));

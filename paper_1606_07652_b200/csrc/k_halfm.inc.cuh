@@ -32,12 +32,16 @@ __device__ __forceinline__ HalfAxes half_block(int blk, int M) {
 // P2M of blocks C / B1 / B2 (blockIdx.y): V[a][b] = sum_j conj(Pa_j[a])
 // (lambda_j conj(Pf_j[f0]) conj(Pb_j[b])); 8 warps = 8 row tiles, all column
 // tiles per warp, the B operand of a 64-point chunk staged in shared memory.
+// NCT column tiles per warp: 8 for block C (M columns), 4 for the B blocks
+// (H - 1 <= 31 columns: the 8-tile loop contracted four all-zero tiles);
+// blk0 + blockIdx.y selects the block.
+template <int NCT>
 __global__ void __launch_bounds__(256, 1)
     k_p2m_axes(const int* __restrict__ leaf_list, const int* __restrict__ leaf_start,
                const double2* __restrict__ pht, const double* __restrict__ lam, int M,
-               long long K, long long n, long long nleaf, double2* __restrict__ mult) {
+               long long K, long long n, long long nleaf, double2* __restrict__ mult, int blk0) {
   extern __shared__ __align__(16) double2 ax_dyn[];  // [kBigPts][64]
-  const HalfAxes hb = half_block(blockIdx.y, M);
+  const HalfAxes hb = half_block(blk0 + blockIdx.y, M);
   const long long lf = leaf_list ? leaf_list[blockIdx.x] : blockIdx.x;
   const int r = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -47,9 +51,9 @@ __global__ void __launch_bounds__(256, 1)
   const int p0 = leaf_start[lf], p1 = leaf_start[lf + 1];
   const double* lr = lam + (long long)r * n;
   const int per = 3 * M;
-  CTile acc[8];
+  CTile acc[NCT];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) acc[u] = CTile{{0.0, 0.0}, {0.0, 0.0}};
+  for (int u = 0; u < NCT; ++u) acc[u] = CTile{{0.0, 0.0}, {0.0, 0.0}};
   for (int c0 = p0; c0 < p1; c0 += kBigPts) {
     const int np = min(kBigPts, p1 - c0);
     __syncthreads();
@@ -68,7 +72,7 @@ __global__ void __launch_bounds__(256, 1)
       if (jv && rv) za = __ldg(pht + (long long)(c0 + j) * per + hb.ax * M + hb.a0 + ra);
       const double are = za.x, aim = -za.y;  // conj(Pa)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < NCT; ++u) {
         const int col = 8 * u + g;
         const double2 b = (jv && col < hb.nb) ? ax_dyn[j * 64 + col] : make_double2(0.0, 0.0);
         cdmma(acc[u], are, aim, -aim, b.x, b.y);
@@ -78,7 +82,7 @@ __global__ void __launch_bounds__(256, 1)
   if (!rv) return;
   double2* out = mult + ((long long)r * nleaf + lf) * K + hb.off + (long long)ra * hb.stride;
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
+  for (int u = 0; u < NCT; ++u)
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       const int col = 8 * u + 2 * tq + v;
